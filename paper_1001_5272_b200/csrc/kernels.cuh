@@ -1,0 +1,277 @@
+// TFT / ITFT / product kernels.
+//
+// Every vector of length n is handled as the first n outputs of the
+// zero-padded power-of-two network (the TFT "prefix property",
+// reference tests/test_transforms.py:89-98), but only n words of it ever live
+// in HBM:
+//
+//  * n <= 2^t_small: one CTA per vector, whole padded tile in shared memory.
+//  * larger n, l = ceil_lg(n) = l0 + l1, C = 2^l1 ("chunk"), R = 2^l0 rows:
+//      forward  A  columns c (stride C, R rows, deep stages, untwisted):
+//                  full padded column transform in smem; rows < n written
+//                  back; the single virtual row K = n>>l1 of columns c >= h
+//                  (h = n mod C) goes to a <= C-word stash.
+//               B  chunks k (contiguous C words, top stages, block twist k):
+//                  the partial last chunk reads its virtual words from the
+//                  stash; only positions < n are stored.
+//      inverse  1  complete chunks k < K: plain inverse.
+//               2  columns c >= h: in-tile ITFT of K rows; their virtual row K
+//                  (sum_i x_i omega_K^i) into the stash.
+//               3  last chunk (one CTA): h known outputs + C-h stashed inputs,
+//                  in-tile generalised ITFT.
+//               4  columns c < h: in-tile ITFT of K+1 rows.
+// The stash is the only extra device memory besides the per-ring twiddle
+// tables (PAPER.md:62 allows O(sqrt n) space for the cache-friendly variant).
+#pragma once
+#include "tile.cuh"
+
+template <typename W>
+struct VecDesc {
+    const int64_t* off;  // per-vector word offset, or null -> stride*v
+    const int64_t* len;  // per-vector length, or null -> n0
+    int64_t stride, n0;
+    TFT_DEV int64_t o(int64_t v) const { return off ? off[v] : stride * v; }
+    TFT_DEV int64_t n(int64_t v) const { return len ? len[v] : n0; }
+};
+
+template <class F>
+struct LaunchArgs {
+    using W = typename F::W;
+    F f;
+    RingDev<W> R;
+    W* x;                 // data vectors (in place)
+    VecDesc<W> xd;
+    const W* in;          // forward input (== x for a transform; A or B for a product)
+    VecDesc<W> ind;       // in_len <= n; positions >= in_len read as 0
+    const W* pre;         // inverse: optional pointwise factor (product: X^ * Y^)
+    W* stash;             // per-vector stash, C words each
+    int l0, l1, wlog;     // two-pass plan (large kernels)
+    int64_t vbase;        // first vector of this launch
+};
+
+template <class F>
+TFT_DEV typename F::W load_pre(const LaunchArgs<F>& a, int64_t idx, typename F::W v) {
+    if (!a.pre) return v;
+    // X^ * Y^ : Montgomery product then * R^2 to undo the R^-1.
+    return a.f.canon(a.f.mont(a.f.red1(a.f.mont(v, a.pre[idx])), a.R.r2.w));
+}
+
+__device__ __forceinline__ int ceil_lg_dev(int64_t n) {
+    return n <= 1 ? 0 : 64 - __clzll((unsigned long long)(n - 1));
+}
+
+// ------------------------------------------------------------ small: 1 CTA/vector
+template <class F>
+__global__ void k_small_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.x;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const int t = ceil_lg_dev(n);
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    SmemTile<W> tl{S, t, 0};
+    for (uint32_t i = threadIdx.x; i < (1u << t); i += blockDim.x) tl.at(i) = i < nin ? in[i] : W(0);
+    __syncthreads();
+    fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
+}
+
+template <class F>
+__global__ void k_small_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.x;
+    const int64_t n = a.xd.n(v);
+    const int t = ceil_lg_dev(n);
+    const int64_t o = a.xd.o(v);
+    W* x = a.x + o;
+    SmemTile<W> tl{S, t, 0};
+    for (uint32_t i = threadIdx.x; i < (1u << t); i += blockDim.x)
+        tl.at(i) = i < n ? load_pre(a, o + i, x[i]) : W(0);
+    __syncthreads();
+    itft_gen(a.f, tl, (uint32_t)n, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
+}
+
+// ------------------------------------------------------------ two-pass, forward
+// grid: (C >> wlog column groups, vectors)
+template <class F>
+__global__ void k_col_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const int l1 = a.l1, l0 = ceil_lg_dev(n) - l1;
+    if (l0 <= 0) return;
+    const uint32_t C = 1u << l1, c0 = blockIdx.x << a.wlog, ncols = 1u << a.wlog;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    SmemTile<W> tl{S, l0, a.wlog};
+    const uint32_t words = tl.words();
+    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
+        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
+        int64_t pos = (int64_t)row * C + c0 + col;
+        tl.at(g) = pos < nin ? in[pos] : W(0);
+    }
+    __syncthreads();
+    fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
+    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
+        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
+        int64_t pos = (int64_t)row * C + c0 + col;
+        if (pos < n) x[pos] = a.f.canon(tl.at(g));
+        else if (h && row == K) a.stash[(v - a.vbase) * (int64_t)C + c0 + col] = a.f.canon(tl.at(g));
+    }
+}
+
+// grid: (max chunks, vectors)
+template <class F>
+__global__ void k_chunk_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1;
+    const uint32_t C = 1u << l1, k = blockIdx.x;
+    if ((int64_t)k * C >= n) return;
+    const uint32_t K = (uint32_t)(n >> l1);
+    W* S = reinterpret_cast<W*>(smem_raw);
+    W* T = S + padded_words(C);
+    W* zeta = T + C;
+    W* x = a.x + a.xd.o(v) + (int64_t)k * C;
+    SmemTile<W> tl{S, l1, 0};
+    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x)
+        tl.at(i) = (k < K || (int64_t)k * C + i < n) ? x[i] : st[i];
+    if (k == 0) {
+        __syncthreads();
+        fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
+    } else {
+        build_heap(a.f, a.R, T, zeta, l1, k, false);
+        fwd_all(a.f, tl, TwHeap<F>{T, l1, a.f});
+    }
+    const uint32_t lim = k < K ? C : (uint32_t)(n - (int64_t)k * C);
+    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
+}
+
+// ------------------------------------------------------------ two-pass, inverse
+// step 1: complete chunks k < K.  grid: (max K, vectors)
+template <class F>
+__global__ void k_chunk_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1;
+    const uint32_t C = 1u << l1, k = blockIdx.x;
+    const uint32_t K = (uint32_t)(n >> l1);
+    if (k >= K) return;
+    W* S = reinterpret_cast<W*>(smem_raw);
+    W* T = S + padded_words(C);
+    W* zeta = T + C;
+    const int64_t o = a.xd.o(v) + (int64_t)k * C;
+    W* x = a.x + o;
+    SmemTile<W> tl{S, l1, 0};
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) tl.at(i) = load_pre(a, o + i, x[i]);
+    if (k == 0) {
+        __syncthreads();
+        inv_all<F, false>(a.f, tl, TwPrefix<F>{a.R.Zi}, C, a.R.ipow2);
+    } else {
+        build_heap(a.f, a.R, T, zeta, l1, k, true);
+        inv_all<F, false>(a.f, tl, TwHeap<F>{T, l1, a.f}, C, a.R.ipow2);
+    }
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
+}
+
+// steps 2 (which = 0: columns c >= h, K rows, stash their row K) and
+// 4 (which = 1: columns c < h, K+1 rows).  grid: (C >> wlog, vectors)
+template <class F>
+__global__ void k_col_inv(LaunchArgs<F> a, int which) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1, l0 = ceil_lg_dev(n) - l1;
+    if (l0 <= 0) return;
+    const uint32_t C = 1u << l1, c0 = blockIdx.x << a.wlog, ncols = 1u << a.wlog;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    // column range of this step
+    const uint32_t lo = which == 0 ? h : 0, hi = which == 0 ? C : h;
+    if (c0 + ncols <= lo || c0 >= hi) return;
+    const uint32_t rows = which == 0 ? K : K + 1;
+    W* S = reinterpret_cast<W*>(smem_raw);
+    SmemTile<W> tl{S, l0, a.wlog};
+    W* red = S + padded_words(tl.words());
+    W* nv = red + blockDim.x;
+    const int64_t o = a.xd.o(v);
+    W* x = a.x + o;
+    const uint32_t words = tl.words();
+    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
+        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
+        int64_t pos = (int64_t)row * C + c0 + col;
+        tl.at(g) = (row < rows && pos < n) ? x[pos] : W(0);
+    }
+    __syncthreads();
+    itft_gen(a.f, tl, rows, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
+    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
+        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
+        uint32_t c = c0 + col;
+        int64_t pos = (int64_t)row * C + c;
+        if (row < rows && c >= lo && c < hi && pos < n) x[pos] = a.f.canon(tl.at(g));
+    }
+    if (which == 0 && h) {
+        // the column's first virtual output z_c[K] = sum_{i<K} x_i omega_K^i
+        colsum_pow(a.f, tl, K, omega_m(a.f, a.R, K), a.R.oneM, red, nv);
+        for (uint32_t col = threadIdx.x; col < ncols; col += blockDim.x) {
+            uint32_t c = c0 + col;
+            if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
+        }
+    }
+}
+
+// step 3: the partial last chunk.  grid: (1, vectors)
+template <class F>
+__global__ void k_last_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1;
+    const uint32_t C = 1u << l1;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    if (!h) return;
+    W* S = reinterpret_cast<W*>(smem_raw);
+    W* Tf = S + padded_words(C);
+    W* Ti = Tf + C;
+    W* zeta = Ti + C;
+    const int64_t o = a.xd.o(v) + (int64_t)K * C;
+    W* x = a.x + o;
+    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    SmemTile<W> tl{S, l1, 0};
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) tl.at(i) = i < h ? load_pre(a, o + i, x[i]) : st[i];
+    if (K == 0) {
+        __syncthreads();
+        itft_gen(a.f, tl, h, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
+    } else {
+        build_heap(a.f, a.R, Tf, zeta, l1, K, false);
+        build_heap(a.f, a.R, Ti, zeta, l1, K, true);
+        itft_gen(a.f, tl, h, TwHeap<F>{Tf, l1, a.f}, TwHeap<F>{Ti, l1, a.f}, a.R);
+    }
+    for (uint32_t i = threadIdx.x; i < h; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
+}
+
+// ------------------------------------------------------------ helpers
+template <typename W>
+__global__ void k_u64_to_w(const uint64_t* __restrict__ s, W* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = (W)s[i];
+}
+template <typename W>
+__global__ void k_w_to_u64(const W* __restrict__ s, uint64_t* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = (uint64_t)s[i];
+}

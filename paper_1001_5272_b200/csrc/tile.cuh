@@ -1,0 +1,358 @@
+// Shared-memory tile engine: one CTA transforms 2^wlog interleaved columns of
+// 2^t words each (column-interleaved: element (pos, col) lives at index
+// pos*2^wlog + col, physical slot idx + idx/32 to break power-of-two bank
+// strides).
+//
+// Network convention (the reference's, `_kernels.pyx:181-223`): forward stage
+// s pairs (u, u + 2^s) with u mod 2^(s+1) < 2^s and multiplies the upper
+// element by theta = omega_{2J}, J = u >> (s+1), global stage order s = t-1
+// .. 0.  A tile that is a sub-block B of a larger transform (positions
+// [B*2^t, (B+1)*2^t) after the stages above it) uses omega_{2(B*2^(t-s-1)+J)};
+// B = 0 is the untwisted case whose twiddles are the prefix Z[0..2^(t-1)) of
+// one size-independent table.
+//
+// Stages run in register rounds of KK <= 5 stages: a thread loads 2^KK
+// words spaced 2^s_lo apart, runs KK butterfly layers in registers and
+// writes them back.  The last forward (first inverse) round always has
+// s_lo = 0 so every round either has s_lo = 0 or s_lo >= 5, which keeps all
+// shared-memory accesses bank-conflict free with the 1-in-32 padding.
+#pragma once
+#include "field.cuh"
+
+template <typename W>
+struct SmemTile {
+    W* S;
+    int t;     // log2 transform length (rows per column)
+    int wlog;  // log2 interleaved columns
+    TFT_DEV W& at(uint32_t idx) const { return S[idx + (idx >> 5)]; }
+    TFT_DEV uint32_t ix(uint32_t pos, uint32_t col) const { return (pos << wlog) | col; }
+    TFT_DEV uint32_t words() const { return 1u << (t + wlog); }
+};
+
+__host__ __device__ inline uint32_t padded_words(uint32_t words) { return words + (words >> 5) + 1; }
+
+// Per-ring device tables (built once per RingConfig by the host).
+template <typename W>
+struct RingDev {
+    const Tw<W>* Zf;    // Zf[j] = omega_{2j},      j < 2^zb
+    const Tw<W>* Zi;    // Zi[j] = omega_{2j}^-1
+    const Tw<W>* Zfh;   // Zfh[i] = omega_{2 i 2^zb}, i < 2^zh
+    const Tw<W>* Zih;
+    const Tw<W>* ipow2; // ipow2[k] = 2^-k, k < 64
+    Tw<W> r2;           // R^2 mod p (Montgomery form of R): mont(x, r2.w) = x R
+    Tw<W> inv2;         // 1/2
+    W oneM;             // R mod p (Montgomery form of 1)
+    int zb, zh;
+};
+
+// omega_{2J} for an arbitrary J < 2^(zb+zh), Montgomery form, canonical.
+template <class F>
+TFT_DEV typename F::W zbig(const F& f, const RingDev<typename F::W>& R, uint64_t J, bool inverse) {
+    const Tw<typename F::W>* lo = inverse ? R.Zi : R.Zf;
+    const Tw<typename F::W>* hi = inverse ? R.Zih : R.Zfh;
+    uint64_t m = (1ull << R.zb) - 1;
+    if (J <= m) return lo[J].w;
+    return f.red1(f.mont(hi[J >> R.zb].w, lo[J & m].w));
+}
+
+// omega_s (modring.py:223-234) in Montgomery form: omega_{2j+1} = -omega_{2j}.
+template <class F>
+TFT_DEV typename F::W omega_m(const F& f, const RingDev<typename F::W>& R, uint64_t s) {
+    typename F::W w = zbig(f, R, s >> 1, false);
+    return (s & 1) ? f.p - w : w;
+}
+
+template <class F>
+TFT_DEV typename F::W pow_m(const F& f, typename F::W baseM, typename F::W oneM, uint64_t e) {
+    typename F::W r = oneM;
+    while (e) {
+        if (e & 1) r = f.red1(f.mont(r, baseM));
+        baseM = f.red1(f.mont(baseM, baseM));
+        e >>= 1;
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------- twiddles
+template <class F>
+struct TwPrefix {  // untwisted tile: theta(s, J) = Z[J]
+    const Tw<typename F::W>* Z;
+    TFT_DEV Tw<typename F::W> get(int, uint32_t J) const { return Z[J]; }
+};
+
+template <class F>
+struct TwHeap {  // twisted tile: stage s table at [2^(t-s-1), 2^(t-s)) of T
+    const typename F::W* T;
+    int t;
+    F f;
+    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
+        return f.mk(T[(1u << (t - s - 1)) + J]);
+    }
+};
+
+// Fill the heap table of block B (level t): T[2^(t-s-1) + J] = omega_{2(B 2^(t-s-1) + J)}
+// = omega_{2 B 2^(t-s-1)} * omega_{2J} (product rule).
+// `zeta` is scratch for t words.  Ends with __syncthreads().
+template <class F>
+TFT_DEV void build_heap(const F& f, const RingDev<typename F::W>& R, typename F::W* T,
+                        typename F::W* zeta, int t, uint64_t B, bool inverse) {
+    using W = typename F::W;
+    for (int s = threadIdx.x; s < t; s += blockDim.x) zeta[s] = zbig(f, R, B << (t - s - 1), inverse);
+    __syncthreads();
+    const Tw<W>* Z = inverse ? R.Zi : R.Zf;
+    for (uint32_t idx = threadIdx.x + 1; idx < (1u << t); idx += blockDim.x) {
+        int lev = 31 - __clz(idx);
+        int s = t - 1 - lev;
+        uint32_t J = idx - (1u << lev);
+        T[idx] = f.red1(f.mont(zeta[s], Z[J].w));
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- rounds
+template <class F, int KK, class TP>
+TFT_DEV void fwd_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, const TP& tp) {
+    using W = typename F::W;
+    const uint32_t cmask = (1u << tl.wlog) - 1;
+    const uint32_t nunits = 1u << (tl.t - KK + tl.wlog);
+    const uint32_t lomask = (1u << s_lo) - 1;
+    for (uint32_t g = threadIdx.x; g < nunits; g += blockDim.x) {
+        uint32_t col = g & cmask, u = g >> tl.wlog;
+        uint32_t base = (u & lomask) | ((u >> s_lo) << (s_lo + KK));
+        W v[1 << KK];
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
+#pragma unroll
+        for (int st = KK - 1; st >= 0; --st) {
+            const int s = s_lo + st;
+            const uint32_t jb = base >> (s + 1);
+#pragma unroll
+            for (int q = 0; q < (1 << (KK - 1 - st)); ++q) {
+                Tw<W> w = tp.get(s, jb + q);
+#pragma unroll
+                for (int r = 0; r < (1 << st); ++r) {
+                    const int i = (q << (st + 1)) | r;
+                    f.fwd(v[i], v[i | (1 << st)], w);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
+    }
+}
+
+// Inverse round, stages s_lo .. s_lo+KK-1 ascending.  With MASK, only pairs
+// inside complete aligned 2^(s+1)-blocks of [0, h) run, and a pair in its
+// block's last stage (u >= h rounded down to 2^(s+2)) is scaled by 2^-(s+1)
+// so every complete block leaves phase 1 holding true (unscaled) values.
+// Without MASK the whole tile is one block and the scale lands at s = t-1.
+template <class F, int KK, bool MASK, class TP>
+TFT_DEV void inv_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, const TP& tp,
+                       uint32_t h, const Tw<typename F::W>* ipow2) {
+    using W = typename F::W;
+    const uint32_t cmask = (1u << tl.wlog) - 1;
+    const uint32_t nunits = 1u << (tl.t - KK + tl.wlog);
+    const uint32_t lomask = (1u << s_lo) - 1;
+    const uint32_t h_lo = MASK ? ((uint32_t)((uint64_t)h >> (s_lo + 1)) << (s_lo + 1)) : 0;
+    for (uint32_t g = threadIdx.x; g < nunits; g += blockDim.x) {
+        uint32_t col = g & cmask, u = g >> tl.wlog;
+        uint32_t base = (u & lomask) | ((u >> s_lo) << (s_lo + KK));
+        if (MASK && base >= h_lo) continue;  // no pair of this unit is active in any stage
+        W v[1 << KK];
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
+#pragma unroll
+        for (int st = 0; st < KK; ++st) {
+            const int s = s_lo + st;
+            const uint32_t jb = base >> (s + 1);
+            const uint32_t hs = MASK ? (uint32_t)(((uint64_t)h >> (s + 1)) << (s + 1)) : 0;
+            const uint32_t hs1 = MASK ? (uint32_t)(((uint64_t)h >> (s + 2)) << (s + 2)) : 0;
+            const bool last_stage = !MASK && (s == tl.t - 1);
+            Tw<W> sc = ipow2[s + 1];
+#pragma unroll
+            for (int q = 0; q < (1 << (KK - 1 - st)); ++q) {
+                Tw<W> w = tp.get(s, jb + q);
+#pragma unroll
+                for (int r = 0; r < (1 << st); ++r) {
+                    const int i = (q << (st + 1)) | r;
+                    const uint32_t pos = base + ((uint32_t)i << s_lo);
+                    if (MASK && pos >= hs) continue;
+                    f.inv(v[i], v[i | (1 << st)], w);
+                    if (MASK ? (pos >= hs1) : last_stage) {
+                        v[i] = f.mulw(v[i], sc);
+                        v[i | (1 << st)] = f.mulw(v[i | (1 << st)], sc);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
+    }
+}
+
+template <class F, class TP>
+TFT_DEV void fwd_round_rt(const F& f, const SmemTile<typename F::W>& tl, int s_lo, int kk, const TP& tp) {
+    switch (kk) {
+        case 1: fwd_round<F, 1>(f, tl, s_lo, tp); break;
+        case 2: fwd_round<F, 2>(f, tl, s_lo, tp); break;
+        case 3: fwd_round<F, 3>(f, tl, s_lo, tp); break;
+        case 4: fwd_round<F, 4>(f, tl, s_lo, tp); break;
+        default: fwd_round<F, 5>(f, tl, s_lo, tp); break;
+    }
+}
+
+template <class F, bool MASK, class TP>
+TFT_DEV void inv_round_rt(const F& f, const SmemTile<typename F::W>& tl, int s_lo, int kk,
+                          const TP& tp, uint32_t h, const Tw<typename F::W>* ipow2) {
+    switch (kk) {
+        case 1: inv_round<F, 1, MASK>(f, tl, s_lo, tp, h, ipow2); break;
+        case 2: inv_round<F, 2, MASK>(f, tl, s_lo, tp, h, ipow2); break;
+        case 3: inv_round<F, 3, MASK>(f, tl, s_lo, tp, h, ipow2); break;
+        case 4: inv_round<F, 4, MASK>(f, tl, s_lo, tp, h, ipow2); break;
+        default: inv_round<F, 5, MASK>(f, tl, s_lo, tp, h, ipow2); break;
+    }
+}
+
+// Full forward transform of every column (all t stages).  Caller has synced
+// after filling the tile; ends synced.
+template <class F, class TP>
+TFT_DEV void fwd_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp) {
+    const int t = tl.t;
+    const int last = t < 5 ? t : 5;
+    int s_hi = t;
+    int first = (t - last) & 3;
+    if (first) {
+        fwd_round_rt(f, tl, s_hi - first, first, tp);
+        s_hi -= first;
+        __syncthreads();
+    }
+    while (s_hi > last) {
+        fwd_round_rt(f, tl, s_hi - 4, 4, tp);
+        s_hi -= 4;
+        __syncthreads();
+    }
+    if (last) {
+        fwd_round_rt(f, tl, 0, last, tp);
+        __syncthreads();
+    }
+}
+
+template <class F, bool MASK, class TP>
+TFT_DEV void inv_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp, uint32_t h,
+                     const Tw<typename F::W>* ipow2) {
+    const int t = tl.t;
+    const int first = t < 5 ? t : 5;
+    if (first) {
+        inv_round_rt<F, MASK>(f, tl, 0, first, tp, h, ipow2);
+        __syncthreads();
+    }
+    int s_lo = first;
+    while (s_lo < t) {
+        int kk = t - s_lo < 4 ? t - s_lo : 4;
+        inv_round_rt<F, MASK>(f, tl, s_lo, kk, tp, h, ipow2);
+        s_lo += kk;
+        __syncthreads();
+    }
+}
+
+// Generalised in-tile inverse (every column at once): slots [0, h) hold
+// transform outputs, slots [h, 2^t) hold KNOWN coefficients (zeros for a plain
+// ITFT, stashed virtual values for the last chunk of a two-pass ITFT).  On
+// return slots [0, h) hold the coefficients; [h, 2^t) are clobbered.
+// This is van der Hoeven's recursive ITFT unrolled into three sweeps:
+//   1. inverse-transform every complete binary block of [0, h) (masked rounds);
+//   2. top-down over levels d (block holding h): either split known tails
+//      into the right half (bit d-1 of h set) or fold them into the left half;
+//   3. bottom-up: recombine the halves with one inverse butterfly.
+// Same values as the reference's Algorithm 2 since the
+// inverse map is unique; the odd-tail Horner passes are not needed.
+template <class F, class TPF, class TPI>
+TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
+                      const TPI& tpi, const RingDev<typename F::W>& R) {
+    using W = typename F::W;
+    const int t = tl.t;
+    const uint32_t ncols = 1u << tl.wlog;
+    inv_all<F, true>(f, tl, tpi, h, R.ipow2);
+    if (h == 0 || h >= (1u << t)) return;
+    const int dlo = __ffs(h);  // levels d with h mod 2^d != 0
+    for (int d = t; d >= dlo; --d) {
+        const uint32_t hd = h & ((1u << d) - 1);
+        const uint32_t B = h - hd, H = 1u << (d - 1);
+        const Tw<W> w = tpf.get(d - 1, B >> d);
+        if (hd >= H) {
+            const uint32_t i0 = hd - H, cnt = (H - i0) << tl.wlog;
+            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
+                uint32_t col = g & (ncols - 1), i = i0 + (g >> tl.wlog);
+                W tv = tl.at(tl.ix(B + H + i, col));
+                W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                W m = f.cmulw(tv, w);
+                W x = f.csub(lo, m);
+                tl.at(tl.ix(B + i, col)) = x;
+                tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
+            }
+        } else {
+            const uint32_t cnt = (H - hd) << tl.wlog;
+            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
+                uint32_t col = g & (ncols - 1), i = hd + (g >> tl.wlog);
+                W a = tl.at(tl.ix(B + i, col));
+                W b = tl.at(tl.ix(B + H + i, col));
+                tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
+            }
+        }
+        __syncthreads();
+    }
+    for (int d = dlo; d <= t; ++d) {
+        const uint32_t hd = h & ((1u << d) - 1);
+        const uint32_t B = h - hd, H = 1u << (d - 1);
+        if (hd >= H) {
+            const Tw<W> wi = tpi.get(d - 1, B >> d);
+            const uint32_t cnt = (hd - H) << tl.wlog;
+            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
+                uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
+                W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                W hi = tl.at(tl.ix(B + H + i, col));
+                tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
+                tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), wi), R.inv2);
+            }
+        } else {
+            const Tw<W> w = tpf.get(d - 1, B >> d);
+            const uint32_t cnt = hd << tl.wlog;
+            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
+                uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
+                W a = tl.at(tl.ix(B + i, col));
+                W b = tl.at(tl.ix(B + H + i, col));
+                tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Per-column evaluation sum_{i<K} S[i] w^i (the first virtual output of a
+// column whose K coefficients are now known).  Result per column into out[col]
+// (canonical).  `red` is scratch of blockDim.x words.  Ends synced.
+template <class F>
+TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t K,
+                        typename F::W wM, typename F::W oneM, typename F::W* red,
+                        typename F::W* out) {
+    using W = typename F::W;
+    const uint32_t ncols = 1u << tl.wlog;
+    const uint32_t nparts = blockDim.x >> tl.wlog;
+    const uint32_t col = threadIdx.x & (ncols - 1), part = threadIdx.x >> tl.wlog;
+    const uint32_t e = (K + nparts - 1) / nparts;
+    const uint32_t r0 = part * e, r1 = min(K, r0 + e);
+    const Tw<W> w = f.mk(wM);
+    W acc = 0;
+    if (r0 < r1) {
+        for (uint32_t i = r1; i-- > r0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(i, col))));
+        acc = f.cmulw(acc, f.mk(pow_m(f, wM, oneM, r0)));
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (part == 0) {
+        W s = 0;
+        for (uint32_t q = 0; q < nparts; ++q) s = f.cadd(s, red[(q << tl.wlog) | col]);
+        out[col] = s;
+    }
+    __syncthreads();
+}

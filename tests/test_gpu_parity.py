@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C ABI) against vectors the
+reference itself produced (tests/golden) and against the oracle, bit-exact.
+Runs on a B200 (`pytest -m gpu`)."""
+
+from array import array
+
+import numpy as np
+import pytest
+
+from conftest import gen, sha
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import paper_1001_5272_b200 as T  # noqa: E402
+from paper_1001_5272_b200 import backend, device  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (checker only)
+
+
+def cfg_for(golden, key):
+    p, top, K = golden["primes"][key]
+    return T.RingConfig(p, top, K)
+
+
+def run(fn, x, cfg):
+    buf = array("Q", np.ascontiguousarray(x, dtype=np.uint64).tobytes())
+    fn(buf, cfg)
+    return np.frombuffer(buf.tobytes(), dtype=np.uint64)
+
+
+def test_known_answers(golden):
+    for case in golden["known"]:
+        cfg = cfg_for(golden, case["prime"])
+        if case["op"] == "tft":
+            buf = T.make_buffer(case["x"], cfg)
+            T.tft(buf, cfg)
+            assert list(buf) == case["y"]
+            T.itft(buf, cfg)
+            assert list(buf) == case["x"]
+        else:
+            x = T.zeros(len(case["a"]) + len(case["b"]) - 1, cfg)
+            T.multiply(T.make_buffer(case["a"], cfg), T.make_buffer(case["b"], cfg), x, cfg)
+            assert list(x) == case["y"]
+
+
+def test_config1(golden):
+    cfg = T.default_config()
+    x = gen(0, cfg.p, 1000)
+    y = run(T.tft, x, cfg)
+    assert sha(y) == golden["config1"]["sha256_u64"]
+    assert np.array_equal(run(T.itft, y, cfg), x)
+
+
+def test_vectors(golden):
+    for case in golden["vectors"]:
+        cfg = cfg_for(golden, case["prime"])
+        x = gen(case["seed_x"], cfg.p, case["n"])
+        y = gen(case["seed_y"], cfg.p, case["n"])
+        assert list(run(T.tft, x, cfg)) == case["tft_x"], (case["prime"], case["n"])
+        assert list(run(T.itft, y, cfg)) == case["itft_y"], (case["prime"], case["n"])
+
+
+def test_digests(golden):
+    for case in golden["digests"]:
+        cfg = cfg_for(golden, case["prime"])
+        x = gen(case["seed_x"], cfg.p, case["n"])
+        y = gen(case["seed_y"], cfg.p, case["n"])
+        fx = run(T.tft, x, cfg)
+        assert sha(fx) == case["tft_x"], ("tft", case["prime"], case["n"], list(fx[:4]), case["tft_x_head"][:4])
+        iy = run(T.itft, y, cfg)
+        assert sha(iy) == case["itft_y"], ("itft", case["prime"], case["n"], list(iy[:4]),
+                                           case["itft_y_head"][:4])
+        assert np.array_equal(run(T.itft, fx, cfg), x)
+
+
+def test_products(golden):
+    for case in golden["products"]:
+        cfg = cfg_for(golden, case["prime"])
+        a = T.make_buffer(case["a"], cfg)
+        b = T.make_buffer(case["b"], cfg)
+        keep = (a.tobytes(), b.tobytes())
+        x = T.zeros(len(a) + len(b) - 1, cfg)
+        T.multiply(a, b, x, cfg)
+        assert list(x) == case["x"]
+        assert (a.tobytes(), b.tobytes()) == keep
+
+
+def test_product_digests(golden):
+    for case in golden["product_digests"]:
+        cfg = cfg_for(golden, case["prime"])
+        g = np.random.default_rng(case["seed"])
+        a = g.integers(0, cfg.p, case["la"], dtype=np.uint64)
+        b = g.integers(0, cfg.p, case["lb"], dtype=np.uint64)
+        x = np.zeros(case["la"] + case["lb"] - 1, dtype=np.uint64)
+        T.multiply(a, b, x, cfg)
+        assert sha(x) == case["x"], (case, list(x[:4]))
+
+
+@pytest.mark.parametrize("key", ["p998244353", "p3221225473", "p4179340454199820289", "p17"])
+def test_every_small_length_against_oracle(golden, key):
+    cfg = cfg_for(golden, key)
+    top = min(1 << cfg.K, 600)
+    for n in range(1, top + 1):
+        x = gen(10_000 + n, cfg.p, n)
+        y = run(T.tft, x, cfg)
+        assert np.array_equal(y, O.tft(x, cfg.p, cfg.omegaK, cfg.K)), n
+        assert np.array_equal(run(T.itft, y, cfg), x), n
+
+
+def test_two_pass_boundaries_against_oracle():
+    cfg = T.default_config()
+    lens = [8191, 8192, 8193, 12289, 16383, 16384, 16385, 32767, 32769, 49153, 65535, 65536, 65537,
+            131071, 131073, 196609, 262143, 262145, 524287, 524289, 1048575, 1048577]
+    for n in lens:
+        x = gen(n, cfg.p, n)
+        y = run(T.tft, x, cfg)
+        assert np.array_equal(y, O.tft(x, cfg.p, cfg.omegaK, cfg.K)), n
+        z = gen(n + 1, cfg.p, n)
+        assert np.array_equal(run(T.itft, z, cfg), O.itft(z, cfg.p, cfg.omegaK, cfg.K)), n
+
+
+def test_fft_pow2_matches_tft():
+    cfg = T.default_config()
+    for k in range(0, 16):
+        x = gen(k, cfg.p, 1 << k)
+        a = run(T.fft_pow2, x, cfg)
+        assert np.array_equal(a, run(T.tft, x, cfg))
+
+
+def test_maximum_size_small_ring():
+    cfg = T.RingConfig(17, 3, 4)
+    x = gen(5, 17, 16)
+    y = run(T.tft, x, cfg)
+    assert np.array_equal(y, O.naive_dft(x, 17, 3, 4))
+    assert np.array_equal(run(T.itft, y, cfg), x)
+
+
+def test_list_buffers_staged():
+    cfg = T.RingConfig(17, 3, 4)
+    buf = [1, 2, 3, 4]
+    T.tft(buf, cfg)
+    assert buf == [10, 15, 6, 7]
+
+
+def test_device_ragged_batch_against_oracle():
+    cfg = T.default_config()
+    rng = np.random.default_rng(1)
+    lens = rng.integers(1, 70000, 24)
+    lens[:4] = [1, 2, 8192, 65536]
+    flat = rng.integers(0, cfg.p, int(lens.sum()), dtype=np.uint64)
+    d = device.to_words(flat, cfg)
+    device.tft_batch_(d, cfg, lengths=lens)
+    got = device.from_words(d, cfg)
+    want = O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K)
+    assert np.array_equal(got, want)
+    device.tft_batch_(d, cfg, lengths=lens, inverse=True)
+    assert np.array_equal(device.from_words(d, cfg), flat)
+
+
+def test_device_uniform_batch_and_products():
+    cfg = T.default_config()
+    rng = np.random.default_rng(2)
+    for n in (1000, 40000):
+        flat = rng.integers(0, cfg.p, 8 * n, dtype=np.uint64)
+        d = device.to_words(flat, cfg)
+        device.tft_batch_(d, cfg, n=n, count=8)
+        want = O.tft_batch(flat, np.full(8, n), cfg.p, cfg.omegaK, cfg.K)
+        assert np.array_equal(device.from_words(d, cfg), want)
+    la, lb, cnt = 3001, 1999, 5
+    a = rng.integers(0, cfg.p, cnt * la, dtype=np.uint64)
+    b = rng.integers(0, cfg.p, cnt * lb, dtype=np.uint64)
+    x = torch.zeros(cnt * (la + lb - 1), dtype=device.word_dtype(cfg), device="cuda")
+    device.multiply_batch(device.to_words(a, cfg), device.to_words(b, cfg), x, cfg, cnt, la, lb)
+    got = device.from_words(x, cfg).reshape(cnt, -1)
+    for v in range(cnt):
+        assert np.array_equal(got[v], O.multiply(a[v * la:(v + 1) * la], b[v * lb:(v + 1) * lb],
+                                                 cfg.p, cfg.omegaK, cfg.K))
+
+
+def test_launches_counted():
+    cfg = T.default_config()
+    backend.launch_count(reset=True)
+    run(T.tft, gen(3, cfg.p, 5000), cfg)
+    assert backend.launch_count() >= 1
