@@ -48,6 +48,15 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
                       uint64_t* x, uint64_t p, uint64_t top, int K, uint64_t inv2,
                       int64_t* mults, int64_t* adds);
 
+/* Batched host-buffer form of tftb_tft_u64 / tftb_itft_u64 (inverse != 0):
+ * `count` vectors inside one host buffer x (uint64 words), vector v at
+ * x + off[v] with length len[v] (host arrays; off == NULL -> back to back).
+ * One H2D copy, one batched device transform, one D2H copy.  The reference
+ * has no batch call — callers thread over buffers (nogil, _kernels.pyx:419);
+ * this is that loop moved onto the device.  Pinned x gives full PCIe rate. */
+int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int64_t count,
+                       uint64_t p, uint64_t top, int K, int inverse);
+
 /* ---------------------------------------------------------------- rings */
 typedef struct tftb_ring tftb_ring;
 
@@ -67,6 +76,17 @@ int tftb_ring_word_bytes(const tftb_ring* ring);
  * Asynchronous w.r.t. the host. */
 int tftb_tft_dev(const tftb_ring* ring, void* data, int64_t count, int64_t n, int64_t stride,
                  const int64_t* h_off, const int64_t* h_len, int inverse, void* stream);
+
+/* Reusable batch plan: the grouping of `count` vectors (same layout
+ * arguments as tftb_tft_dev) by kernel plan, with its device-side offset /
+ * length arrays and scratch allocated once.  Executing a plan issues only
+ * kernel launches (no host synchronisation), so it can be captured in a
+ * CUDA graph. */
+typedef struct tftb_plan tftb_plan;
+int tftb_plan_create(const tftb_ring* ring, int64_t count, int64_t n, int64_t stride,
+                     const int64_t* h_off, const int64_t* h_len, tftb_plan** out);
+int tftb_plan_execute(const tftb_plan* plan, void* data, int inverse, void* stream);
+int tftb_plan_destroy(tftb_plan* plan);
 
 /* Products of `count` pairs: x_v[0:la+lb-1) = a_v * b_v.  a_v = a + v*sa,
  * b_v = b + v*sb, x_v = x + v*sx (device words, ring word type).  `scratch`

@@ -10,18 +10,21 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "tftb200.cu")
+UNITS = ["tftb200.cu", "inst_f30.cu", "inst_f32.cu", "inst_f62.cu"]
 OUT = os.path.join(HERE, "libtftb200.so")
 STAMP = OUT + ".stamp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+OBJ = os.path.join(HERE, "csrc", "_obj")
 
 
 def _digest():
     h = hashlib.sha256(" ".join(FLAGS).encode())
     for d in (os.path.join(HERE, "csrc"), os.path.join(ROOT, "include")):
         for name in sorted(os.listdir(d)):
+            if os.path.isdir(os.path.join(d, name)):
+                continue
             with open(os.path.join(d, name), "rb") as f:
                 h.update(name.encode() + f.read())
     return h.hexdigest()
@@ -33,12 +36,25 @@ def build(force=False, verbose=False):
         with open(STAMP) as f:
             if f.read().strip() == dig:
                 return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, SRC]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = res.stdout + res.stderr
+    os.makedirs(OBJ, exist_ok=True)
+    procs = []
+    for u in UNITS:
+        obj = os.path.join(OBJ, u.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, "-c", "-o", obj, os.path.join(HERE, "csrc", u)]
+        procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    log, failed = "", False
+    for obj, pr in procs:
+        out, _ = pr.communicate()
+        log += f"==== {obj}\n{out}"
+        failed |= pr.returncode != 0
+    if not failed:
+        link = subprocess.run([NVCC, "-shared", "-o", OUT, *[o for o, _ in procs], "-lcudart"],
+                              capture_output=True, text=True)
+        log += link.stdout + link.stderr
+        failed = link.returncode != 0
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:
         f.write(log)
-    if res.returncode != 0:
+    if failed:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed building libtftb200.so")
     if verbose:

@@ -1,0 +1,322 @@
+// One thread-block cluster per vector for 2^CL < n <= 8 * 2^CL (config 2's
+// 2^15 < n <= 2^16 lives here): CTA g of a G-CTA cluster owns chunk g =
+// positions [g*2^CL, (g+1)*2^CL) in shared memory, so a transform touches HBM
+// exactly once each way (BASELINE.md §5 passes_min = 1).
+//
+// Forward: the top gam = ceil_lg(n) - CL stages of the network pair words in
+// different chunks; they run as 2^gam-point "column" transforms, one thread
+// per column reading and writing the G chunks through distributed shared
+// memory (columns are independent, so a column's owner thread is its only
+// reader and writer).  The remaining CL stages are local to each chunk (the
+// chunk is sub-block g of the network; its twiddles are the size-independent
+// omega_{2J} at global J).  Chunks past n are never materialised: their input
+// words are zero and their outputs are not needed.
+//
+// Inverse (K = n >> CL complete chunks, h = n mod 2^CL):
+//   1. chunks g < K: plain inverse of all CL local stages;
+//   2. columns c >= h: K known outputs -> K coefficients by V_K^-1, and the
+//      column's next output sum_j x_j omega_K^j written into chunk K slot c;
+//   3. chunk K: generalised in-tile inverse with h known outputs and the
+//      2^CL - h values from step 2 as its known tail;
+//   4. columns c < h: K+1 known outputs -> coefficients by V_{K+1}^-1.
+// This is the two-level form of the inverse; values equal the
+// reference's Algorithm 2 because the inverse map is unique.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+// Direct twiddles for a tile that is block `blk` at level T:
+// theta(s, J) = omega_{2 (blk 2^(T-s-1) + J)} read from the w-only table.
+template <class F>
+struct TwDirect {
+    const typename F::W* Zw;
+    uint32_t blk;
+    int T;
+    F f;
+    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
+        return f.mk(__ldg(Zw + ((blk << (T - s - 1)) + J)));
+    }
+    // N consecutive twiddles from an N-aligned index (true for every call in
+    // reg_fwd / reg_inv), with 16-byte loads where the word type allows
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
+        using W = typename F::W;
+        const W* p = Zw + ((blk << (T - s - 1)) + J0);
+        constexpr int V = 16 / sizeof(W);
+        if constexpr (N >= V && V > 1) {
+#pragma unroll
+            for (int q = 0; q < N; q += V) {
+                if constexpr (sizeof(W) == 4) {
+                    uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
+                    out[q] = f.mk(t.x);
+                    out[q + 1] = f.mk(t.y);
+                    out[q + 2] = f.mk(t.z);
+                    out[q + 3] = f.mk(t.w);
+                } else {
+                    ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + q));
+                    out[q] = f.mk(t.x);
+                    out[q + 1] = f.mk(t.y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < N; ++q) out[q] = f.mk(__ldg(p + q));
+        }
+    }
+};
+
+// ------------------------------------------------------ compile-time rounds
+template <int SLO>
+struct PhysStep {
+    static constexpr uint32_t v = SLO >= 5 ? (1u << SLO) + (1u << (SLO - 5)) : (1u << SLO);
+};
+
+template <class F, int TL, int KK, int SLO, class TP>
+TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp) {
+    using W = typename F::W;
+    constexpr uint32_t NU = 1u << (TL - KK);
+    constexpr uint32_t STEP = PhysStep<SLO>::v;
+    for (uint32_t u = threadIdx.x; u < NU; u += blockDim.x) {
+        const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
+        W* pb = S + base + (base >> 5);
+        W v[1 << KK];
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
+        reg_fwd<F, KK, KK - 1>(f, v, base, SLO, tp);
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
+    }
+}
+
+// unmasked inverse round; the tile's last stage (s = TL-1) also scales by 2^-TL
+template <class F, int TL, int KK, int SLO, bool MASK, class TP>
+TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
+                          uint32_t h) {
+    using W = typename F::W;
+    constexpr uint32_t NU = 1u << (TL - KK);
+    constexpr uint32_t STEP = PhysStep<SLO>::v;
+    const uint32_t h_lo = MASK ? (uint32_t)(((uint64_t)h >> (SLO + 1)) << (SLO + 1)) : 0;
+    for (uint32_t u = threadIdx.x; u < NU; u += blockDim.x) {
+        const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
+        if (MASK && base >= h_lo) continue;
+        W* pb = S + base + (base >> 5);
+        W v[1 << KK];
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
+        reg_inv<F, KK, 0, MASK>(f, v, base, SLO, tp, h, TL - 1, ipow2);
+#pragma unroll
+        for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
+    }
+}
+
+// stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),
+// recursing down to a final 5-or-fewer-stage round at s_lo = 0.
+template <class F, int TL, int SHI, class TP>
+TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp) {
+    if constexpr (SHI <= 5) {
+        fwd_round_ct<F, TL, SHI, 0>(f, S, tp);
+        __syncthreads();
+    } else {
+        constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
+        fwd_round_ct<F, TL, KK, SHI - KK>(f, S, tp);
+        __syncthreads();
+        fwd_rounds_ct<F, TL, SHI - KK>(f, S, tp);
+    }
+}
+
+template <class F, int TL, int SHI, bool MASK, class TP>
+TFT_DEV void inv_rounds_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
+                           uint32_t h = 0) {
+    if constexpr (SHI <= 5) {
+        inv_round_ct<F, TL, SHI, 0, MASK>(f, S, tp, ipow2, h);
+        __syncthreads();
+    } else {
+        constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
+        inv_rounds_ct<F, TL, SHI - KK, MASK>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, KK, SHI - KK, MASK>(f, S, tp, ipow2, h);
+        __syncthreads();
+    }
+}
+
+// this CTA's share [lo, hi) of the columns [c0, C), 32-aligned
+__device__ __forceinline__ void col_share(uint32_t c0, uint32_t C, uint32_t g, uint32_t G, uint32_t& lo,
+                                          uint32_t& hi) {
+    const uint32_t span = C - c0;
+    lo = c0 + ((uint32_t)(((uint64_t)span * g / G)) & ~31u);
+    hi = g + 1 == G ? C : c0 + ((uint32_t)(((uint64_t)span * (g + 1) / G)) & ~31u);
+    if (g == 0) lo = c0;
+}
+
+// the 2^GAM-point column network of the top GAM stages, one thread per column;
+// rows j >= G are past n (zero in, dropped out)
+template <class F, int GAM>
+TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint32_t g, uint32_t G, uint32_t C,
+                       const typename F::W* Zw) {
+    using W = typename F::W;
+    constexpr int GP = 1 << GAM;
+    W* rs[GP];
+#pragma unroll
+    for (int j = 0; j < GP; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
+    Tw<W> tw[GP / 2 > 0 ? GP / 2 : 1];
+#pragma unroll
+    for (int j = 0; j < GP / 2; ++j) tw[j] = f.mk(__ldg(Zw + j));
+    uint32_t lo, hi;
+    col_share(0, C, g, G, lo, hi);
+    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+        const uint32_t ph = c + (c >> 5);
+        W col[GP];
+#pragma unroll
+        for (int j = 0; j < GP; ++j) col[j] = j < (int)G ? rs[j][ph] : W(0);
+#pragma unroll
+        for (int sp = GAM - 1; sp >= 0; --sp) {
+#pragma unroll
+            for (int j = 0; j < GP; ++j) {
+                if ((j >> sp) & 1) continue;
+                f.fwd(col[j], col[j + (1 << sp)], tw[j >> (sp + 1)]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < GP; ++j)
+            if (j < (int)G) rs[j][ph] = col[j];
+    }
+}
+
+// ------------------------------------------------------------ kernels
+template <class F, int CL>
+__global__ void __launch_bounds__(256, 3) k_cl_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t g = cl.block_rank(), G = cl.num_blocks();
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const int gam = ceil_lg_dev(n) - CL;
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    const F f = a.f;
+
+    const int64_t cbase = (int64_t)g * C;
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
+        const int64_t pos = cbase + i;
+        S[i + (i >> 5)] = pos < nin ? in[pos] : W(0);
+    }
+    cl.sync();
+
+    // cross stages: 2^gam-point untwisted column transforms over DSMEM
+    switch (gam) {
+        case 1: cross_fwd<F, 1>(f, cl, S, g, G, C, a.R.Zwf); break;
+        case 2: cross_fwd<F, 2>(f, cl, S, g, G, C, a.R.Zwf); break;
+        default: cross_fwd<F, 3>(f, cl, S, g, G, C, a.R.Zwf); break;
+    }
+    cl.sync();
+
+    fwd_rounds_ct<F, CL, CL>(f, S, TwDirect<F>{a.R.Zwf, g, CL, f});
+
+    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
+    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
+}
+
+// column solve: rows j < M of column `ph` (physical index) hold the column's
+// first M outputs; replace them by its M coefficients (V_M^-1, M^2 products);
+// optionally write the next output sum_j x_j omega_M^j into row M.
+template <class F, int M>
+TFT_DEV void col_solve_m(const F& f, typename F::W* const* rs, uint32_t ph, const Tw<typename F::W>* blk,
+                         bool write_next) {
+    using W = typename F::W;
+    W y[M], xv[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) y[j] = f.canon(rs[j][ph]);
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        W acc = 0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(y[c], blk[8 * r + c]));
+        xv[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < M; ++r) rs[r][ph] = xv[r];
+    if (write_next) {
+        W acc = 0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(xv[c], blk[64 + c]));
+        rs[M][ph] = acc;
+    }
+}
+
+template <class F, int M>
+TFT_DEV void col_solve_range(const F& f, typename F::W* const* rs, uint32_t lo, uint32_t hi,
+                             const Tw<typename F::W>* blk, bool write_next) {
+    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) col_solve_m<F, M>(f, rs, c + (c >> 5), blk, write_next);
+}
+
+template <class F>
+TFT_DEV void col_solve(const F& f, typename F::W* const* rs, uint32_t lo, uint32_t hi, int m,
+                       const Tw<typename F::W>* blk, bool write_next) {
+    switch (m) {
+        case 1: col_solve_range<F, 1>(f, rs, lo, hi, blk, write_next); break;
+        case 2: col_solve_range<F, 2>(f, rs, lo, hi, blk, write_next); break;
+        case 3: col_solve_range<F, 3>(f, rs, lo, hi, blk, write_next); break;
+        case 4: col_solve_range<F, 4>(f, rs, lo, hi, blk, write_next); break;
+        case 5: col_solve_range<F, 5>(f, rs, lo, hi, blk, write_next); break;
+        case 6: col_solve_range<F, 6>(f, rs, lo, hi, blk, write_next); break;
+        case 7: col_solve_range<F, 7>(f, rs, lo, hi, blk, write_next); break;
+        default: col_solve_range<F, 8>(f, rs, lo, hi, blk, write_next); break;
+    }
+}
+
+template <class F, int CL>
+__global__ void __launch_bounds__(256, 3) k_cl_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t g = cl.block_rank(), G = cl.num_blocks();
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    const int64_t o = a.xd.o(v);
+    W* x = a.x + o;
+    const F f = a.f;
+    const int64_t cbase = (int64_t)g * C;
+
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
+        const int64_t pos = cbase + i;
+        S[i + (i >> 5)] = pos < n ? load_pre(a, o + pos, x[pos]) : W(0);
+    }
+    __syncthreads();
+    // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
+    // known outputs [0, h), never the tail the columns will fill) alongside
+    const TwDirect<F> tpi{a.R.Zwi, g, CL, f};
+    if (g < K) inv_rounds_ct<F, CL, CL, false>(f, S, tpi, a.R.ipow2);
+    else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+    cl.sync();
+
+    W* rs[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
+    {
+        uint32_t lo, hi;
+        col_share(h, C, g, G, lo, hi);
+        col_solve(f, rs, lo, hi, (int)K, a.R.vinv + 72 * (K - 1), h != 0);
+    }
+    cl.sync();
+    if (h && g == K) {
+        SmemTile<W> tl{S, CL, 0};
+        itft_phases23(f, tl, h, TwDirect<F>{a.R.Zwf, K, CL, f}, tpi, a.R);
+    }
+    cl.sync();
+    if (h) {
+        uint32_t lo, hi;
+        col_share(0, h, g, G, lo, hi);
+        col_solve(f, rs, lo, hi, (int)K + 1, a.R.vinv + 72 * K, false);
+    }
+    cl.sync();
+    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
+    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
+}

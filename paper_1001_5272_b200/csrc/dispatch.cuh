@@ -1,0 +1,213 @@
+// Batch planning and launches (instantiated once per field type).
+#pragma once
+#include "cluster.cuh"
+#include "host.h"
+
+namespace tftb {
+
+// One group of vectors that share a plan.
+template <class F>
+int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, const typename F::W* pre,
+              int64_t count, VecDesc<typename F::W> xd, VecDesc<typename F::W> ind, int64_t maxn,
+              bool inverse, cudaStream_t st, typename F::W* stash_buf = nullptr) {
+    using W = typename F::W;
+    Plan pl;
+    if (make_plan<F>(maxn, &pl)) return -1;
+    LaunchArgs<F> a{};
+    a.f = make_field<F>(rh->p);
+    a.R = ring_dev<F>(rh);
+    a.x = x;
+    a.xd = xd;
+    a.in = in ? in : x;
+    a.ind = in ? ind : xd;
+    a.pre = pre;
+    a.l0 = pl.l0;
+    a.l1 = pl.l1;
+    a.wlog = pl.wlog;
+    if (pl.kind == kCluster) {
+        constexpr int CL = Limits<F>::CL;
+        const size_t smem = padded_words(1u << CL) * sizeof(W);
+        if (set_smem(k_cl_fwd<F, CL>, smem) || set_smem(k_cl_inv<F, CL>, smem)) return -1;
+        for (int64_t v0 = 0; v0 < count; v0 += 65535) {
+            a.vbase = v0;
+            unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(pl.G, nv, 1);
+            lc.blockDim = dim3(kNT, 1, 1);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = pl.G;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            if (inverse) CK(cudaLaunchKernelEx(&lc, k_cl_inv<F, CL>, a));
+            else CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F, CL>, a));
+            g_launches++;
+        }
+        return 0;
+    }
+    if (pl.kind == kSmall) {
+        size_t smem = padded_words(1u << pl.l) * sizeof(W);
+        int nt = std::max(32, std::min(kNT, (1 << pl.l) / 16));
+        if (inverse) {
+            if (set_smem(k_small_inv<F>, smem)) return -1;
+        } else {
+            if (set_smem(k_small_fwd<F>, smem)) return -1;
+        }
+        for (int64_t v0 = 0; v0 < count; v0 += (1ll << 30)) {
+            a.vbase = v0;
+            unsigned nb = (unsigned)std::min<int64_t>(count - v0, 1ll << 30);
+            if (inverse) k_small_inv<F><<<nb, nt, smem, st>>>(a);
+            else k_small_fwd<F><<<nb, nt, smem, st>>>(a);
+            g_launches++;
+            CK(cudaGetLastError());
+        }
+        return 0;
+    }
+    const uint32_t C = 1u << pl.l1;
+    const int64_t maxchunks = (maxn + C - 1) / C;
+    const int64_t vchunk = 65535;
+    Scratch stash;
+    if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
+    a.stash = stash_buf ? stash_buf : (W*)stash.p;
+    const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 64) * sizeof(W);
+    const size_t sm_chunk = (padded_words(C) + C + 64) * sizeof(W);
+    const size_t sm_last = (padded_words(C) + 2 * C + 64) * sizeof(W);
+    if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F>, sm_chunk) ||
+        set_smem(k_chunk_inv<F>, sm_chunk) || set_smem(k_last_inv<F>, sm_last))
+        return -1;
+    for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
+        a.vbase = v0;
+        unsigned nv = (unsigned)std::min(count - v0, vchunk);
+        dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
+        if (!inverse) {
+            k_col_fwd<F><<<gcol, kNT, sm_col, st>>>(a);
+            k_chunk_fwd<F><<<gchunk, kNT, sm_chunk, st>>>(a);
+            g_launches += 2;
+        } else {
+            k_chunk_inv<F><<<gchunk, kNT, sm_chunk, st>>>(a);
+            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
+            k_last_inv<F><<<glast, kNT, sm_last, st>>>(a);
+            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
+            g_launches += 4;
+        }
+        CK(cudaGetLastError());
+    }
+    return 0;
+}
+
+// Build a reusable batch plan: vectors grouped by kernel plan, per-group
+// device offset/length arrays and the largest stash, all allocated once.
+template <class F>
+int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                const int64_t* h_len, PlanImpl* P) {
+    using W = typename F::W;
+    P->rh = rh;
+    P->count = count;
+    std::map<int, std::vector<int64_t>> groups;
+    for (int64_t v = 0; v < count; v++) {
+        int64_t nv = h_len ? h_len[v] : n;
+        if (nv <= 0) return fail("vector length must be positive");
+        Plan pl;
+        if (make_plan<F>(nv, &pl)) return -1;
+        groups[pl.key()].push_back(v);
+    }
+    size_t words = 0, stash_words = 0;
+    for (auto& kv : groups) {
+        PlanGroup g;
+        g.count = (int64_t)kv.second.size();
+        g.maxn = 0;
+        std::vector<int64_t> off(g.count), len(g.count);
+        for (int64_t i = 0; i < g.count; i++) {
+            int64_t v = kv.second[i];
+            off[i] = h_off ? h_off[v] : v * stride;
+            len[i] = h_len ? h_len[v] : n;
+            g.maxn = std::max(g.maxn, len[i]);
+        }
+        Plan pl;
+        make_plan<F>(g.maxn, &pl);
+        if (pl.kind == kLarge)
+            stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << pl.l1);
+        g.arr_off = words;
+        words += 2 * g.count;
+        P->host_arrays.insert(P->host_arrays.end(), off.begin(), off.end());
+        P->host_arrays.insert(P->host_arrays.end(), len.begin(), len.end());
+        P->groups.push_back(g);
+    }
+    CK(cudaMalloc(&P->darr, std::max<size_t>(words, 1) * sizeof(int64_t)));
+    CK(cudaMemcpy(P->darr, P->host_arrays.data(), words * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (stash_words) CK(cudaMalloc(&P->stash, stash_words * sizeof(W)));
+    return 0;
+}
+
+template <class F>
+int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st) {
+    using W = typename F::W;
+    for (const auto& g : P->groups) {
+        const int64_t* d = (const int64_t*)P->darr + g.arr_off;
+        VecDesc<W> xd{d, d + g.count, 0, 0};
+        if (run_group<F>(P->rh, (W*)data, nullptr, (const W*)pre, g.count, xd, xd, g.maxn, inverse != 0, st,
+                         (W*)P->stash))
+            return -1;
+    }
+    return 0;
+}
+
+// Partition a batch by plan (ceil_lg of the length class) and run each group.
+template <class F>
+int run_batch(const RingHost* rh, void* data, const void* in, int64_t count, int64_t n, int64_t stride,
+              const int64_t* h_off, const int64_t* h_len, const void* in_data, int64_t in_n,
+              int64_t in_stride, const void* pre, bool inverse, cudaStream_t st) {
+    using W = typename F::W;
+    if (count <= 0) return 0;
+    if (!h_off && !h_len) {
+        VecDesc<W> xd{nullptr, nullptr, stride, n};
+        VecDesc<W> ind{nullptr, nullptr, in_stride, in_n};
+        return run_group<F>(rh, (W*)data, (const W*)in_data, (const W*)pre, count, xd, ind, n, inverse, st);
+    }
+    (void)in;
+    PlanImpl P;
+    if (plan_create<F>(rh, count, n, stride, h_off, h_len, &P)) return -1;
+    int rc = plan_exec<F>(&P, data, inverse, pre, st);
+    CK(cudaStreamSynchronize(st));  // the temporary plan's arrays die here
+    return rc;
+}
+
+template <class F>
+int dispatch_tft(const RingHost* rh, void* data, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                 const int64_t* h_len, int inverse, cudaStream_t st) {
+    return run_batch<F>(rh, data, nullptr, count, n, stride, h_off, h_len, nullptr, 0, 0, nullptr, inverse != 0, st);
+}
+
+template <class F>
+int dispatch_mul(const RingHost* rh, const void* a, int64_t la, int64_t sa, const void* b, int64_t lb, int64_t sb,
+                 void* x, int64_t sx, int64_t count, void* scratch, cudaStream_t st) {
+    using W = typename F::W;
+    const int64_t r = la + lb - 1;
+    if (sx != r) return fail("multiply_dev: output stride must equal la+lb-1");
+    Scratch own;
+    if (!scratch) {
+        if (own.get((size_t)count * r * sizeof(W), st)) return -1;
+        scratch = own.p;
+    }
+    // X_v <- TFT_r(a_v || 0), Y_v <- TFT_r(b_v || 0), X_v <- ITFT_r(X_v * Y_v)
+    if (run_batch<F>(rh, x, nullptr, count, r, sx, nullptr, nullptr, a, la, sa, nullptr, false, st)) return -1;
+    if (run_batch<F>(rh, scratch, nullptr, count, r, r, nullptr, nullptr, b, lb, sb, nullptr, false, st)) return -1;
+    if (run_batch<F>(rh, x, nullptr, count, r, sx, nullptr, nullptr, nullptr, 0, 0, scratch, true, st)) return -1;
+    return 0;
+}
+
+
+}  // namespace tftb
+
+#define TFTB_INSTANTIATE(F)                                                                                   \
+    template int tftb::plan_create<F>(const RingHost*, int64_t, int64_t, int64_t, const int64_t*, const int64_t*, \
+                                      PlanImpl*);                                                               \
+    template int tftb::plan_exec<F>(const PlanImpl*, void*, int, const void*, cudaStream_t);                  \
+    template int tftb::dispatch_tft<F>(const RingHost*, void*, int64_t, int64_t, int64_t, const int64_t*,     \
+                                       const int64_t*, int, cudaStream_t);                                      \
+    template int tftb::dispatch_mul<F>(const RingHost*, const void*, int64_t, int64_t, const void*, int64_t, \
+                                       int64_t, void*, int64_t, int64_t, void*, cudaStream_t);

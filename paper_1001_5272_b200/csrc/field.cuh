@@ -9,11 +9,13 @@
 //         uint64 words, Harvey lazy butterflies (4p < 2^64).
 //
 // Twiddles are stored in Montgomery form wM = w*R mod p (R = 2^32 or 2^64)
-// together with wMp = wM * p^-1 mod R, so b*w mod p costs three integer
-// multiplies and no division:
-//   m = b*wMp (low word), r = hi(b*wM) - hi(m*p) (+p)
-// because hi(b*wM) and hi(m*p) have equal low words.  For any word b and
-// canonical w the result lies in (0, 2p); F32 folds it back to [0, p).
+// together with a companion wMp = wM * (+-p^-1) mod R, so b*w mod p costs
+// three integer multiplies and no division (Montgomery reduction with the
+// quotient digit m = lo(b*wM) * (+-p^-1) = b*wMp precomputed per twiddle):
+//   F30:      m = b*wMp, r = (b*wM + m*p) >> 32          (companion -p^-1)
+//   F32/F62:  m = b*wMp, r = hi(b*wM) - hi(m*p) (+p)      (companion +p^-1)
+// both exact because the low words cancel.  Results lie in [0, 2p); F32
+// folds back to [0, p).
 // Reference: the scalar `(u128)a*b % p` of `_kernels.pyx:17-18`.
 #pragma once
 #include <cstdint>
@@ -29,23 +31,25 @@ struct Tw {
 struct F30 {
     using W = uint32_t;
     static constexpr bool kLazy = true;
-    W p, p2, pinv;
+    W p, p2, pinv;  // pinv holds -p^-1 mod 2^32 for this field (REDC sign)
 
     TFT_DEV W red2(W x) const { return min(x, x - p2); }  // [0,4p) -> [0,2p)
     TFT_DEV W red1(W x) const { return min(x, x - p); }   // [0,2p) -> [0,p)
     TFT_DEV W canon(W x) const { return red1(red2(x)); }
-    // b * w for any 32-bit b: (0, 2p)
+    // b * w for any b < 4p: REDC of T = b*wM with m = b*wMp = lo(T)*(-p^-1):
+    // (T + m p) / 2^32 in [0, 2p).  Written as one 64-bit sum so ptxas emits
+    // IMAD, IMAD.WIDE and one IMAD.HI with the 64-bit addend (no negations).
     TFT_DEV W mulw(W b, W wM, W wMp) const {
-        W hi = __umulhi(b, wM);
-        W m = b * wMp;
-        return hi - __umulhi(m, p) + p;
+        const uint32_t m = b * wMp;
+        const uint64_t t = (uint64_t)b * wM + (uint64_t)m * p;
+        return (W)(t >> 32);
     }
     TFT_DEV W mulw(W b, Tw<W> t) const { return mulw(b, t.w, t.wp); }
-    // Montgomery product a*b/R for a*b < p*R: (0, 2p)
+    // Montgomery product a*b/R for a, b < 2p: [0, 2p)
     TFT_DEV W mont(W a, W b) const {
-        W hi = __umulhi(a, b);
-        W m = a * b * pinv;
-        return hi - __umulhi(m, p) + p;
+        const uint64_t ab = (uint64_t)a * b;
+        const uint32_t m = (uint32_t)ab * pinv;
+        return (W)((ab + (uint64_t)m * p) >> 32);
     }
     TFT_DEV Tw<W> mk(W wM) const { return Tw<W>{wM, wM * pinv}; }
     // Cooley-Tukey (DIT on the remainder tree) butterfly: (a + w b, a - w b).

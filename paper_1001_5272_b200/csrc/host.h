@@ -1,0 +1,211 @@
+// Host-side declarations shared by the libtftb200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <vector>
+
+#include "tile.cuh"
+
+namespace tftb {
+
+
+typedef unsigned __int128 u128;
+
+extern thread_local std::string g_err;
+extern thread_local int64_t g_launches;
+
+inline int fail(const std::string& msg) {
+    g_err = msg;
+    return -1;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) return fail(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)((u128)a * b % p); }
+inline uint64_t powmod(uint64_t a, uint64_t e, uint64_t p) {
+    uint64_t r = 1 % p;
+    a %= p;
+    while (e) {
+        if (e & 1) r = mulmod(r, a, p);
+        a = mulmod(a, a, p);
+        e >>= 1;
+    }
+    return r;
+}
+inline int ceil_lg(int64_t n) {
+    int k = 0;
+    while (((int64_t)1 << k) < n) k++;
+    return k;
+}
+
+// -------------------------------------------------------------- ring tables
+struct RingHost {
+    uint64_t p, top;
+    int K;
+    int wbytes;      // 4 or 8
+    int kind;        // 0 F30, 1 F32, 2 F62
+    int zb, zh;
+    void* dmem = nullptr;  // one allocation for every table
+    RingDev<uint32_t> r32{};
+    RingDev<uint64_t> r64{};
+    ~RingHost() {
+        if (dmem) cudaFree(dmem);
+    }
+};
+
+template <typename W>
+W inv_word(W p) {  // p^-1 mod 2^bits (Newton)
+    W x = p;
+    for (int i = 0; i < 7; i++) x *= (W)2 - p * x;
+    return x;
+}
+
+template <class F>
+F make_field(uint64_t p) {
+    F f;
+    f.p = (typename F::W)p;
+    f.p2 = (typename F::W)(2 * p);
+    f.pinv = inv_word<typename F::W>((typename F::W)p);
+    if (std::is_same<F, F30>::value) f.pinv = (typename F::W)(0u - f.pinv);  // F30 uses the REDC sign
+    return f;
+}
+
+template <class F>
+const RingDev<typename F::W>& ring_dev(const RingHost* rh);
+template <>
+inline const RingDev<uint32_t>& ring_dev<F30>(const RingHost* rh) { return rh->r32; }
+template <>
+inline const RingDev<uint32_t>& ring_dev<F32>(const RingHost* rh) { return rh->r32; }
+template <>
+inline const RingDev<uint64_t>& ring_dev<F62>(const RingHost* rh) { return rh->r64; }
+
+// -------------------------------------------------------------- planning
+constexpr int kNT = 256;
+
+template <class F>
+struct Limits {
+    // log2 words of one CTA's shared-memory chunk (64 KB) and of the column tiles
+    static constexpr int CL = sizeof(typename F::W) == 4 ? 14 : 13;
+    static constexpr int col_t = sizeof(typename F::W) == 4 ? 13 : 12;
+    static constexpr int chunk_max = sizeof(typename F::W) == 4 ? 15 : 14;
+};
+
+enum PlanKind { kSmall = 0, kCluster = 1, kLarge = 2 };
+
+struct Plan {
+    PlanKind kind;
+    int l, l0, l1, wlog, G;
+    int key() const { return kind == kSmall ? -1 : (kind == kCluster ? 1000 + G : l); }
+};
+
+template <class F>
+int make_plan(int64_t n, Plan* pl) {
+    const int l = ceil_lg(n);
+    pl->l = l;
+    pl->l0 = pl->l1 = pl->wlog = 0;
+    pl->G = 1;
+    const int CL = Limits<F>::CL;
+    if (l <= CL) {
+        pl->kind = kSmall;
+        return 0;
+    }
+    if (n <= (8ll << CL)) {
+        pl->kind = kCluster;
+        pl->G = (int)((n + (1ll << CL) - 1) >> CL);
+        return 0;
+    }
+    pl->kind = kLarge;
+    int l0 = std::min(l / 2, Limits<F>::col_t - 4);
+    int l1 = l - l0;
+    if (l1 > Limits<F>::chunk_max) {
+        l1 = Limits<F>::chunk_max;
+        l0 = l - l1;
+    }
+    int wlog = std::max(1, std::min(4, Limits<F>::col_t - l0));
+    if (l0 + wlog > Limits<F>::col_t + 1) return fail("transform length too large for the two-pass plan");
+    pl->l0 = l0;
+    pl->l1 = l1;
+    pl->wlog = wlog;
+    return 0;
+}
+
+template <class K_>
+int set_smem(K_ kern, size_t bytes) {
+    // one attribute call per (kernel, device) for the largest size seen
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    if (bytes <= 48 * 1024) return 0;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[{(const void*)kern, dev}];
+    if (bytes <= cur) return 0;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+    return 0;
+}
+
+struct Scratch {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    int get(size_t b, cudaStream_t st) {
+        s = st;
+        if (b == 0) return 0;
+        CK(cudaMallocAsync(&p, b, st));
+        bytes = b;
+        return 0;
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+
+struct PlanGroup {
+    int64_t count, maxn;
+    size_t arr_off;  // offsets then lengths, in darr
+};
+
+struct PlanImpl {
+    const RingHost* rh = nullptr;
+    int64_t count = 0;
+    std::vector<PlanGroup> groups;
+    std::vector<int64_t> host_arrays;
+    void* darr = nullptr;
+    void* stash = nullptr;
+    ~PlanImpl() {
+        if (darr) cudaFree(darr);
+        if (stash) cudaFree(stash);
+    }
+};
+
+template <class F>
+int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                const int64_t* h_len, PlanImpl* P);
+template <class F>
+int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st);
+
+// defined per field in inst_f30.cu / inst_f32.cu / inst_f62.cu
+template <class F>
+int dispatch_tft(const RingHost* rh, void* data, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                 const int64_t* h_len, int inverse, cudaStream_t st);
+template <class F>
+int dispatch_mul(const RingHost* rh, const void* a, int64_t la, int64_t sa, const void* b, int64_t lb, int64_t sb,
+                 void* x, int64_t sx, int64_t count, void* scratch, cudaStream_t st);
+
+}  // namespace tftb

@@ -1,0 +1,4 @@
+// F62 instantiation of the batch dispatch (compiled as its own unit).
+#include "dispatch.cuh"
+
+TFTB_INSTANTIATE(F62)

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -13,57 +14,13 @@
 #include <vector>
 
 #include "../../include/tftb200.h"
+#include "host.h"
 #include "kernels.cuh"
 
-namespace {
-
-typedef unsigned __int128 u128;
+namespace tftb {
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
-
-int fail(const std::string& msg) {
-    g_err = msg;
-    return -1;
-}
-
-#define CK(call)                                                                        \
-    do {                                                                                \
-        cudaError_t e_ = (call);                                                        \
-        if (e_ != cudaSuccess) return fail(std::string(#call) + ": " + cudaGetErrorString(e_)); \
-    } while (0)
-
-uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)((u128)a * b % p); }
-uint64_t powmod(uint64_t a, uint64_t e, uint64_t p) {
-    uint64_t r = 1 % p;
-    a %= p;
-    while (e) {
-        if (e & 1) r = mulmod(r, a, p);
-        a = mulmod(a, a, p);
-        e >>= 1;
-    }
-    return r;
-}
-int ceil_lg(int64_t n) {
-    int k = 0;
-    while (((int64_t)1 << k) < n) k++;
-    return k;
-}
-
-// -------------------------------------------------------------- ring tables
-struct RingHost {
-    uint64_t p, top;
-    int K;
-    int wbytes;      // 4 or 8
-    int kind;        // 0 F30, 1 F32, 2 F62
-    int zb, zh;
-    void* dmem = nullptr;  // one allocation for every table
-    RingDev<uint32_t> r32{};
-    RingDev<uint64_t> r64{};
-    ~RingHost() {
-        if (dmem) cudaFree(dmem);
-    }
-};
 
 template <typename W>
 struct TableBuilder {
@@ -79,16 +36,12 @@ struct TableBuilder {
 };
 
 template <typename W>
-W inv_word(W p) {  // p^-1 mod 2^bits (Newton)
-    W x = p;
-    for (int i = 0; i < 7; i++) x *= (W)2 - p * x;
-    return x;
-}
-
-template <typename W>
 int build_tables(RingHost* rh, RingDev<W>* out) {
     const uint64_t p = rh->p;
-    TableBuilder<W> tb{p, (int)(8 * sizeof(W)), inv_word<W>((W)p), 0};
+    // companion = wM * pinv, with pinv = -p^-1 for the F30 (REDC) field
+    W pinv = inv_word<W>((W)p);
+    if (rh->kind == 0) pinv = (W)(0u - pinv);
+    TableBuilder<W> tb{p, (int)(8 * sizeof(W)), pinv, 0};
     // omega_[k] = top^(2^(K-k))
     std::vector<uint64_t> lvl(rh->K + 1), ilvl(rh->K + 1);
     uint64_t itop = powmod(rh->top, p - 2, p);
@@ -116,7 +69,7 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     build(lvl, zfh, zb);
     build(ilvl, zih, zb);
     std::vector<Tw<W>> host;
-    host.reserve(2 * nz + 2 * nh + 64);
+    host.reserve(2 * nz + 2 * nh + 64 + 8 * 72);
     for (auto v : zf) host.push_back(tb.tw(v));
     for (auto v : zi) host.push_back(tb.tw(v));
     for (auto v : zfh) host.push_back(tb.tw(v));
@@ -126,14 +79,65 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
         host.push_back(tb.tw(ip));
         ip = mulmod(ip, inv2, p);
     }
-    CK(cudaMalloc(&rh->dmem, host.size() * sizeof(Tw<W>)));
-    CK(cudaMemcpy(rh->dmem, host.data(), host.size() * sizeof(Tw<W>), cudaMemcpyHostToDevice));
+    // small-column solvers: V_m^-1 for the first m points omega_0..omega_{m-1}
+    // (V_m[s][i] = omega_s^i) and the next-point row omega_m^i, m = 1..8
+    auto omega_s = [&](uint64_t sidx) -> uint64_t {
+        if (sidx == 0) return 1;
+        int k = 64 - __builtin_clzll(sidx);
+        uint64_t r = 0, t = sidx;
+        for (int i = 0; i < k; i++) { r = (r << 1) | (t & 1); t >>= 1; }
+        return k <= rh->K ? powmod(lvl[k], r, p) : 0;
+    };
+    for (int m = 1; m <= 8; m++) {
+        std::vector<uint64_t> A(m * 2 * m, 0);
+        for (int r = 0; r < m; r++) {
+            uint64_t w = omega_s(r), pw = 1;
+            for (int c = 0; c < m; c++) { A[r * 2 * m + c] = pw; pw = mulmod(pw, w, p); }
+            A[r * 2 * m + m + r] = 1;
+        }
+        bool ok = (int)rh->K >= (m > 1 ? 64 - __builtin_clzll((uint64_t)(m - 1)) : 0);
+        for (int c = 0; c < m && ok; c++) {  // Gauss-Jordan mod p
+            int piv = -1;
+            for (int r = c; r < m; r++) if (A[r * 2 * m + c]) { piv = r; break; }
+            if (piv < 0) { ok = false; break; }
+            for (int k = 0; k < 2 * m; k++) std::swap(A[c * 2 * m + k], A[piv * 2 * m + k]);
+            uint64_t inv = powmod(A[c * 2 * m + c], p - 2, p);
+            for (int k = 0; k < 2 * m; k++) A[c * 2 * m + k] = mulmod(A[c * 2 * m + k], inv, p);
+            for (int r = 0; r < m; r++) {
+                if (r == c || !A[r * 2 * m + c]) continue;
+                uint64_t f = A[r * 2 * m + c];
+                for (int k = 0; k < 2 * m; k++)
+                    A[r * 2 * m + k] = (A[r * 2 * m + k] + p - mulmod(f, A[c * 2 * m + k], p)) % p;
+            }
+        }
+        for (int r = 0; r < 8; r++)
+            for (int c = 0; c < 8; c++)
+                host.push_back(tb.tw(ok && r < m && c < m ? A[r * 2 * m + m + c] : 0));
+        uint64_t wn = omega_s(m), pw = 1;
+        for (int c = 0; c < 8; c++) {
+            host.push_back(tb.tw(ok && c < m ? pw : 0));
+            pw = mulmod(pw, wn, p);
+        }
+    }
+    size_t tw_bytes = host.size() * sizeof(Tw<W>);
+    CK(cudaMalloc(&rh->dmem, tw_bytes + 2 * nz * sizeof(W)));
+    CK(cudaMemcpy(rh->dmem, host.data(), tw_bytes, cudaMemcpyHostToDevice));
+    std::vector<W> words(2 * nz);
+    for (size_t j = 0; j < nz; j++) {
+        words[j] = host[j].w;
+        words[nz + j] = host[nz + j].w;
+    }
+    W* dw = (W*)((char*)rh->dmem + tw_bytes);
+    CK(cudaMemcpy(dw, words.data(), 2 * nz * sizeof(W), cudaMemcpyHostToDevice));
     Tw<W>* d = (Tw<W>*)rh->dmem;
     out->Zf = d;
     out->Zi = d + nz;
     out->Zfh = d + 2 * nz;
     out->Zih = d + 2 * nz + nh;
     out->ipow2 = d + 2 * nz + 2 * nh;
+    out->vinv = d + 2 * nz + 2 * nh + 64;
+    out->Zwf = dw;
+    out->Zwi = dw + nz;
     uint64_t R1 = tb.to_m(1);
     out->r2 = tb.tw(R1);  // Montgomery form of R is R^2 mod p
     out->inv2 = tb.tw(inv2);
@@ -165,232 +169,13 @@ int get_ring(uint64_t p, uint64_t top, int K, RingHost** out) {
     rh->wbytes = p < (1ull << 32) ? 4 : 8;
     rh->kind = p < (1ull << 30) ? 0 : (p < (1ull << 32) ? 1 : 2);
     int km1 = K > 0 ? K - 1 : 0;
-    rh->zb = std::min(km1, 14);
+    rh->zb = std::min(km1, 16);
     rh->zh = std::min(km1 - rh->zb, 16);
     int rc = rh->wbytes == 4 ? build_tables<uint32_t>(rh.get(), &rh->r32)
                              : build_tables<uint64_t>(rh.get(), &rh->r64);
     if (rc) return rc;
     *out = rh.get();
     g_rings[key] = std::move(rh);
-    return 0;
-}
-
-template <class F>
-F make_field(uint64_t p) {
-    F f;
-    f.p = (typename F::W)p;
-    f.p2 = (typename F::W)(2 * p);
-    f.pinv = inv_word<typename F::W>((typename F::W)p);
-    return f;
-}
-
-template <class F>
-const RingDev<typename F::W>& ring_dev(const RingHost* rh);
-template <>
-const RingDev<uint32_t>& ring_dev<F30>(const RingHost* rh) { return rh->r32; }
-template <>
-const RingDev<uint32_t>& ring_dev<F32>(const RingHost* rh) { return rh->r32; }
-template <>
-const RingDev<uint64_t>& ring_dev<F62>(const RingHost* rh) { return rh->r64; }
-
-// -------------------------------------------------------------- planning
-constexpr int kNT = 256;
-
-template <class F>
-struct Limits {
-    // log2 words of the single-vector tile and of the column / chunk tiles
-    static constexpr int small_t = sizeof(typename F::W) == 4 ? 13 : 12;
-    static constexpr int col_t = sizeof(typename F::W) == 4 ? 13 : 12;
-    static constexpr int chunk_max = sizeof(typename F::W) == 4 ? 15 : 14;
-};
-
-struct Plan {
-    bool small;
-    int l, l0, l1, wlog;
-};
-
-template <class F>
-int make_plan(int l, Plan* pl) {
-    pl->l = l;
-    if (l <= Limits<F>::small_t) {
-        pl->small = true;
-        pl->l0 = pl->l1 = pl->wlog = 0;
-        return 0;
-    }
-    pl->small = false;
-    int l0 = std::min(l / 2, Limits<F>::col_t - 4);
-    int l1 = l - l0;
-    if (l1 > Limits<F>::chunk_max) {
-        l1 = Limits<F>::chunk_max;
-        l0 = l - l1;
-    }
-    int wlog = std::max(1, std::min(4, Limits<F>::col_t - l0));
-    if (l0 + wlog > Limits<F>::col_t + 1) return fail("transform length too large for the two-pass plan");
-    pl->l0 = l0;
-    pl->l1 = l1;
-    pl->wlog = wlog;
-    return 0;
-}
-
-template <class K_>
-int set_smem(K_ kern, size_t bytes) {
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    return 0;
-}
-
-struct Scratch {
-    void* p = nullptr;
-    size_t bytes = 0;
-    cudaStream_t s = nullptr;
-    int get(size_t b, cudaStream_t st) {
-        s = st;
-        if (b == 0) return 0;
-        CK(cudaMallocAsync(&p, b, st));
-        bytes = b;
-        return 0;
-    }
-    ~Scratch() {
-        if (p) cudaFreeAsync(p, s);
-    }
-};
-
-// One group of vectors that share a plan.
-template <class F>
-int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, const typename F::W* pre,
-              int64_t count, VecDesc<typename F::W> xd, VecDesc<typename F::W> ind, int64_t maxn,
-              bool inverse, cudaStream_t st) {
-    using W = typename F::W;
-    Plan pl;
-    if (make_plan<F>(ceil_lg(maxn), &pl)) return -1;
-    LaunchArgs<F> a{};
-    a.f = make_field<F>(rh->p);
-    a.R = ring_dev<F>(rh);
-    a.x = x;
-    a.xd = xd;
-    a.in = in ? in : x;
-    a.ind = in ? ind : xd;
-    a.pre = pre;
-    a.l0 = pl.l0;
-    a.l1 = pl.l1;
-    a.wlog = pl.wlog;
-    if (pl.small) {
-        size_t smem = padded_words(1u << pl.l) * sizeof(W);
-        int nt = std::max(32, std::min(kNT, (1 << pl.l) / 16));
-        if (inverse) {
-            if (set_smem(k_small_inv<F>, smem)) return -1;
-        } else {
-            if (set_smem(k_small_fwd<F>, smem)) return -1;
-        }
-        for (int64_t v0 = 0; v0 < count; v0 += (1ll << 30)) {
-            a.vbase = v0;
-            unsigned nb = (unsigned)std::min<int64_t>(count - v0, 1ll << 30);
-            if (inverse) k_small_inv<F><<<nb, nt, smem, st>>>(a);
-            else k_small_fwd<F><<<nb, nt, smem, st>>>(a);
-            g_launches++;
-            CK(cudaGetLastError());
-        }
-        return 0;
-    }
-    const uint32_t C = 1u << pl.l1;
-    const int64_t maxchunks = (maxn + C - 1) / C;
-    const int64_t vchunk = 65535;
-    Scratch stash;
-    if (stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
-    a.stash = (W*)stash.p;
-    const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 64) * sizeof(W);
-    const size_t sm_chunk = (padded_words(C) + C + 64) * sizeof(W);
-    const size_t sm_last = (padded_words(C) + 2 * C + 64) * sizeof(W);
-    if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F>, sm_chunk) ||
-        set_smem(k_chunk_inv<F>, sm_chunk) || set_smem(k_last_inv<F>, sm_last))
-        return -1;
-    for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
-        a.vbase = v0;
-        unsigned nv = (unsigned)std::min(count - v0, vchunk);
-        dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
-        if (!inverse) {
-            k_col_fwd<F><<<gcol, kNT, sm_col, st>>>(a);
-            k_chunk_fwd<F><<<gchunk, kNT, sm_chunk, st>>>(a);
-            g_launches += 2;
-        } else {
-            k_chunk_inv<F><<<gchunk, kNT, sm_chunk, st>>>(a);
-            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
-            k_last_inv<F><<<glast, kNT, sm_last, st>>>(a);
-            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
-            g_launches += 4;
-        }
-        CK(cudaGetLastError());
-    }
-    return 0;
-}
-
-// Partition a batch by plan (ceil_lg of the length class) and run each group.
-template <class F>
-int run_batch(const RingHost* rh, void* data, const void* in, int64_t count, int64_t n, int64_t stride,
-              const int64_t* h_off, const int64_t* h_len, const void* in_data, int64_t in_n,
-              int64_t in_stride, const void* pre, bool inverse, cudaStream_t st) {
-    using W = typename F::W;
-    if (count <= 0) return 0;
-    if (!h_off && !h_len) {
-        VecDesc<W> xd{nullptr, nullptr, stride, n};
-        VecDesc<W> ind{nullptr, nullptr, in_stride, in_n};
-        return run_group<F>(rh, (W*)data, (const W*)in_data, (const W*)pre, count, xd, ind, n, inverse, st);
-    }
-    (void)in;
-    // group vectors by the plan they need
-    std::map<int, std::vector<int64_t>> groups;
-    for (int64_t v = 0; v < count; v++) {
-        int64_t nv = h_len ? h_len[v] : n;
-        if (nv <= 0) return fail("vector length must be positive");
-        int l = ceil_lg(nv);
-        Plan pl;
-        if (make_plan<F>(l, &pl)) return -1;
-        int key = pl.small ? -1 : l;  // one small group (t varies per vector inside the kernel)
-        groups[key].push_back(v);
-    }
-    for (auto& kv : groups) {
-        auto& idx = kv.second;
-        std::vector<int64_t> off(idx.size()), len(idx.size());
-        int64_t maxn = 0;
-        for (size_t i = 0; i < idx.size(); i++) {
-            off[i] = h_off ? h_off[idx[i]] : idx[i] * stride;
-            len[i] = h_len ? h_len[idx[i]] : n;
-            maxn = std::max(maxn, len[i]);
-        }
-        Scratch d;
-        if (d.get(2 * idx.size() * sizeof(int64_t), st)) return -1;
-        int64_t* doff = (int64_t*)d.p;
-        CK(cudaMemcpyAsync(doff, off.data(), idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(doff + idx.size(), len.data(), idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-        VecDesc<W> xd{doff, doff + idx.size(), 0, 0};
-        if (run_group<F>(rh, (W*)data, nullptr, (const W*)pre, (int64_t)idx.size(), xd, xd, maxn, inverse, st))
-            return -1;
-        // host vectors off/len must outlive the async copies
-        CK(cudaStreamSynchronize(st));
-    }
-    return 0;
-}
-
-template <class F>
-int dispatch_tft(const RingHost* rh, void* data, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
-                 const int64_t* h_len, int inverse, cudaStream_t st) {
-    return run_batch<F>(rh, data, nullptr, count, n, stride, h_off, h_len, nullptr, 0, 0, nullptr, inverse != 0, st);
-}
-
-template <class F>
-int dispatch_mul(const RingHost* rh, const void* a, int64_t la, int64_t sa, const void* b, int64_t lb, int64_t sb,
-                 void* x, int64_t sx, int64_t count, void* scratch, cudaStream_t st) {
-    using W = typename F::W;
-    const int64_t r = la + lb - 1;
-    if (sx != r) return fail("multiply_dev: output stride must equal la+lb-1");
-    Scratch own;
-    if (!scratch) {
-        if (own.get((size_t)count * r * sizeof(W), st)) return -1;
-        scratch = own.p;
-    }
-    // X_v <- TFT_r(a_v || 0), Y_v <- TFT_r(b_v || 0), X_v <- ITFT_r(X_v * Y_v)
-    if (run_batch<F>(rh, x, nullptr, count, r, sx, nullptr, nullptr, a, la, sa, nullptr, false, st)) return -1;
-    if (run_batch<F>(rh, scratch, nullptr, count, r, r, nullptr, nullptr, b, lb, sb, nullptr, false, st)) return -1;
-    if (run_batch<F>(rh, x, nullptr, count, r, sx, nullptr, nullptr, nullptr, 0, 0, scratch, true, st)) return -1;
     return 0;
 }
 
@@ -435,7 +220,10 @@ int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, boo
     return 0;
 }
 
-}  // namespace
+}  // namespace tftb
+
+using namespace tftb;
+
 
 // ====================================================================== C ABI
 extern "C" {
@@ -497,6 +285,48 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     return 0;
 }
 
+int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int64_t count, uint64_t p,
+                       uint64_t top, int K, int inverse) {
+    if (count <= 0) return 0;
+    if (!len) return fail("len must not be NULL");
+    RingHost* rh;
+    if (get_ring(p, top, K, &rh)) return -1;
+    std::vector<int64_t> o(count);
+    int64_t lo = INT64_MAX, hi = 0, acc = 0;
+    for (int64_t v = 0; v < count; v++) {
+        if (len[v] <= 0 || (K < 62 && len[v] > (1ll << K))) return fail("vector length outside [1, 2^K]");
+        o[v] = off ? off[v] : acc;
+        acc += len[v];
+        lo = std::min(lo, o[v]);
+        hi = std::max(hi, o[v] + len[v]);
+    }
+    const int64_t span = hi - lo;
+    for (auto& e : o) e -= lo;
+    cudaStream_t st = nullptr;
+    const size_t wb = rh->wbytes;
+    Scratch buf;
+    if (buf.get((size_t)span * 8 + (wb == 4 ? (size_t)span * 4 : 0), st)) return -1;
+    uint64_t* d64 = (uint64_t*)buf.p;
+    CK(cudaMemcpyAsync(d64, x + lo, (size_t)span * 8, cudaMemcpyHostToDevice, st));
+    int rc;
+    int nb = (int)std::min<int64_t>((span + 255) / 256, 148 * 16);
+    if (wb == 4) {
+        uint32_t* dw = (uint32_t*)(d64 + span);
+        k_u64_to_w<uint32_t><<<nb, 256, 0, st>>>(d64, dw, span);
+        rc = rh->kind == 0 ? dispatch_tft<F30>(rh, dw, count, 0, 0, o.data(), len, inverse, st)
+                           : dispatch_tft<F32>(rh, dw, count, 0, 0, o.data(), len, inverse, st);
+        if (rc) return rc;
+        k_w_to_u64<uint32_t><<<nb, 256, 0, st>>>(dw, d64, span);
+        g_launches += 2;
+    } else {
+        rc = dispatch_tft<F62>(rh, d64, count, 0, 0, o.data(), len, inverse, st);
+        if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(x + lo, d64, (size_t)span * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
 struct tftb_ring {
     RingHost* h;
 };
@@ -525,6 +355,41 @@ int tftb_tft_dev(const tftb_ring* ring, void* data, int64_t count, int64_t n, in
         case 1: return dispatch_tft<F32>(rh, data, count, n, stride, h_off, h_len, inverse, st);
         default: return dispatch_tft<F62>(rh, data, count, n, stride, h_off, h_len, inverse, st);
     }
+}
+
+struct tftb_plan {
+    PlanImpl impl;
+    int kind;
+};
+
+int tftb_plan_create(const tftb_ring* ring, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                     const int64_t* h_len, tftb_plan** out) {
+    if (!ring || !out) return fail("null ring / out");
+    if (count <= 0) return fail("plan needs at least one vector");
+    const RingHost* rh = ring->h;
+    std::unique_ptr<tftb_plan> pl(new tftb_plan());
+    pl->kind = rh->kind;
+    int rc = rh->kind == 0 ? plan_create<F30>(rh, count, n, stride, h_off, h_len, &pl->impl)
+             : rh->kind == 1 ? plan_create<F32>(rh, count, n, stride, h_off, h_len, &pl->impl)
+                             : plan_create<F62>(rh, count, n, stride, h_off, h_len, &pl->impl);
+    if (rc) return rc;
+    *out = pl.release();
+    return 0;
+}
+
+int tftb_plan_execute(const tftb_plan* plan, void* data, int inverse, void* stream) {
+    if (!plan) return fail("null plan");
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (plan->kind) {
+        case 0: return plan_exec<F30>(&plan->impl, data, inverse, nullptr, st);
+        case 1: return plan_exec<F32>(&plan->impl, data, inverse, nullptr, st);
+        default: return plan_exec<F62>(&plan->impl, data, inverse, nullptr, st);
+    }
+}
+
+int tftb_plan_destroy(tftb_plan* plan) {
+    delete plan;
+    return 0;
 }
 
 int tftb_multiply_dev(const tftb_ring* ring, const void* a, int64_t la, int64_t sa, const void* b, int64_t lb,

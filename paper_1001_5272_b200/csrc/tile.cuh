@@ -39,6 +39,10 @@ struct RingDev {
     const Tw<W>* Zfh;   // Zfh[i] = omega_{2 i 2^zb}, i < 2^zh
     const Tw<W>* Zih;
     const Tw<W>* ipow2; // ipow2[k] = 2^-k, k < 64
+    const W* Zwf;       // Montgomery words of Zf / Zi alone (companion recomputed
+    const W* Zwi;       //   with one multiply: halves twiddle traffic)
+    const Tw<W>* vinv;  // 8 blocks of 72: V_m^-1 (m x m, V_m[s][i] = omega_s^i), then omega_m^i
+
     Tw<W> r2;           // R^2 mod p (Montgomery form of R): mont(x, r2.w) = x R
     Tw<W> inv2;         // 1/2
     W oneM;             // R mod p (Montgomery form of 1)
@@ -78,6 +82,11 @@ template <class F>
 struct TwPrefix {  // untwisted tile: theta(s, J) = Z[J]
     const Tw<typename F::W>* Z;
     TFT_DEV Tw<typename F::W> get(int, uint32_t J) const { return Z[J]; }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
+#pragma unroll
+        for (int q = 0; q < N; ++q) out[q] = Z[J0 + q];
+    }
 };
 
 template <class F>
@@ -88,7 +97,67 @@ struct TwHeap {  // twisted tile: stage s table at [2^(t-s-1), 2^(t-s)) of T
     TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
         return f.mk(T[(1u << (t - s - 1)) + J]);
     }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
+#pragma unroll
+        for (int q = 0; q < N; ++q) out[q] = get(s, J0 + q);
+    }
 };
+
+// ------------------------------------------------ in-register butterfly layers
+// A unit holds 2^KK words v[i] at positions base + i*2^slo.  Layer ST (stage
+// s = slo + ST) pairs (i, i + 2^ST) with twiddle index (base >> (s+1)) + q,
+// q = i >> (ST+1).  Template recursion keeps every index a compile-time
+// constant so the unit stays in registers.
+template <class F, int KK, int ST, class TP>
+TFT_DEV void reg_fwd(const F& f, typename F::W* v, uint32_t base, int slo, const TP& tp) {
+    using W = typename F::W;
+    constexpr int NQ = 1 << (KK - 1 - ST);
+    const int s = slo + ST;
+    Tw<W> w[NQ];
+    tp.template get_many<NQ>(s, base >> (s + 1), w);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+        for (int r = 0; r < (1 << ST); ++r) {
+            const int i = (q << (ST + 1)) | r;
+            f.fwd(v[i], v[i | (1 << ST)], w[q]);
+        }
+    }
+    if constexpr (ST > 0) reg_fwd<F, KK, ST - 1>(f, v, base, slo, tp);
+}
+
+// ascending layers ST .. KK-1; pairs with pos >= lim[s] are skipped (MASK) and
+// pairs with pos >= scl[s] (or, unmasked, the layer at s == last) are scaled
+template <class F, int KK, int ST, bool MASK, class TP>
+TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const TP& tp, uint32_t h, int last,
+                     const Tw<typename F::W>* ipow2) {
+    using W = typename F::W;
+    constexpr int NQ = 1 << (KK - 1 - ST);
+    const int s = slo + ST;
+    Tw<W> w[NQ];
+    tp.template get_many<NQ>(s, base >> (s + 1), w);
+    const uint32_t hs = MASK ? (uint32_t)(((uint64_t)h >> (s + 1)) << (s + 1)) : 0;
+    const uint32_t hs1 = MASK ? (uint32_t)(((uint64_t)h >> (s + 2)) << (s + 2)) : 0;
+    const bool scale_all = !MASK && s == last;
+    Tw<W> sc;
+    if (MASK || scale_all) sc = ipow2[s + 1];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+        for (int r = 0; r < (1 << ST); ++r) {
+            const int i = (q << (ST + 1)) | r;
+            const uint32_t pos = base + ((uint32_t)i << slo);
+            if (MASK && pos >= hs) continue;
+            f.inv(v[i], v[i | (1 << ST)], w[q]);
+            if (MASK ? pos >= hs1 : scale_all) {
+                v[i] = f.mulw(v[i], sc);
+                v[i | (1 << ST)] = f.mulw(v[i | (1 << ST)], sc);
+            }
+        }
+    }
+    if constexpr (ST + 1 < KK) reg_inv<F, KK, ST + 1, MASK>(f, v, base, slo, tp, h, last, ipow2);
+}
 
 // Fill the heap table of block B (level t): T[2^(t-s-1) + J] = omega_{2(B 2^(t-s-1) + J)}
 // = omega_{2 B 2^(t-s-1)} * omega_{2J} (product rule).
@@ -122,20 +191,7 @@ TFT_DEV void fwd_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, 
         W v[1 << KK];
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
-#pragma unroll
-        for (int st = KK - 1; st >= 0; --st) {
-            const int s = s_lo + st;
-            const uint32_t jb = base >> (s + 1);
-#pragma unroll
-            for (int q = 0; q < (1 << (KK - 1 - st)); ++q) {
-                Tw<W> w = tp.get(s, jb + q);
-#pragma unroll
-                for (int r = 0; r < (1 << st); ++r) {
-                    const int i = (q << (st + 1)) | r;
-                    f.fwd(v[i], v[i | (1 << st)], w);
-                }
-            }
-        }
+        reg_fwd<F, KK, KK - 1>(f, v, base, s_lo, tp);
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
     }
@@ -161,30 +217,7 @@ TFT_DEV void inv_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, 
         W v[1 << KK];
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
-#pragma unroll
-        for (int st = 0; st < KK; ++st) {
-            const int s = s_lo + st;
-            const uint32_t jb = base >> (s + 1);
-            const uint32_t hs = MASK ? (uint32_t)(((uint64_t)h >> (s + 1)) << (s + 1)) : 0;
-            const uint32_t hs1 = MASK ? (uint32_t)(((uint64_t)h >> (s + 2)) << (s + 2)) : 0;
-            const bool last_stage = !MASK && (s == tl.t - 1);
-            Tw<W> sc = ipow2[s + 1];
-#pragma unroll
-            for (int q = 0; q < (1 << (KK - 1 - st)); ++q) {
-                Tw<W> w = tp.get(s, jb + q);
-#pragma unroll
-                for (int r = 0; r < (1 << st); ++r) {
-                    const int i = (q << (st + 1)) | r;
-                    const uint32_t pos = base + ((uint32_t)i << s_lo);
-                    if (MASK && pos >= hs) continue;
-                    f.inv(v[i], v[i | (1 << st)], w);
-                    if (MASK ? (pos >= hs1) : last_stage) {
-                        v[i] = f.mulw(v[i], sc);
-                        v[i | (1 << st)] = f.mulw(v[i | (1 << st)], sc);
-                    }
-                }
-            }
-        }
+        reg_inv<F, KK, 0, MASK>(f, v, base, s_lo, tp, h, tl.t - 1, ipow2);
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
     }
@@ -267,12 +300,11 @@ TFT_DEV void inv_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp
 // Same values as the reference's Algorithm 2 since the
 // inverse map is unique; the odd-tail Horner passes are not needed.
 template <class F, class TPF, class TPI>
-TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
+TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
                       const TPI& tpi, const RingDev<typename F::W>& R) {
     using W = typename F::W;
     const int t = tl.t;
     const uint32_t ncols = 1u << tl.wlog;
-    inv_all<F, true>(f, tl, tpi, h, R.ipow2);
     if (h == 0 || h >= (1u << t)) return;
     const int dlo = __ffs(h);  // levels d with h mod 2^d != 0
     for (int d = t; d >= dlo; --d) {
@@ -326,6 +358,13 @@ TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h,
         }
         __syncthreads();
     }
+}
+
+template <class F, class TPF, class TPI>
+TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
+                      const TPI& tpi, const RingDev<typename F::W>& R) {
+    inv_all<F, true>(f, tl, tpi, h, R.ipow2);
+    itft_phases23(f, tl, h, tpf, tpi, R);
 }
 
 // Per-column evaluation sum_{i<K} S[i] w^i (the first virtual output of a

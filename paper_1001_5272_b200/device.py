@@ -99,3 +99,38 @@ def multiply_batch(a, b, x, cfg, count, la, lb, scratch=None, stream=None):
                                                    ctypes.c_void_p(x.data_ptr()), r, count, sp,
                                                    _stream(stream)))
     return x
+
+
+class BatchPlan:
+    """A reusable grouping of a ragged batch (tftb_plan_*): build once, then
+    execute() issues only kernel launches on the given stream."""
+
+    def __init__(self, cfg, lengths, offsets=None):
+        ln = np.ascontiguousarray(lengths, dtype=np.int64)
+        if (ln <= 0).any() or (ln > (1 << cfg.K)).any():
+            raise ValueError("vector lengths must lie in [1, 2^K]")
+        of = np.ascontiguousarray(offsets if offsets is not None else np.concatenate(([0], np.cumsum(ln)[:-1])),
+                                  dtype=np.int64)
+        self.cfg = cfg
+        self.count = int(ln.size)
+        self.span = int((of + ln).max()) if ln.size else 0
+        self._lib = backend.load()
+        self._h = ctypes.c_void_p()
+        backend.check(self._lib.tftb_plan_create(backend.ring_handle(cfg), self.count, 0, 0,
+                                                 of.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                 ln.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                 ctypes.byref(self._h)))
+
+    def execute(self, data, inverse=False, stream=None):
+        _check_words(data, self.cfg)
+        if data.numel() < self.span:
+            raise ValueError("buffer smaller than the plan's vectors")
+        backend.check(self._lib.tftb_plan_execute(self._h, ctypes.c_void_p(data.data_ptr()),
+                                                  1 if inverse else 0, _stream(stream)))
+        return data
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.tftb_plan_destroy(h)
+            self._h = None

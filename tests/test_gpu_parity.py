@@ -183,3 +183,19 @@ def test_launches_counted():
     backend.launch_count(reset=True)
     run(T.tft, gen(3, cfg.p, 5000), cfg)
     assert backend.launch_count() >= 1
+
+
+def test_batch_plan_reuse_against_oracle():
+    cfg = T.default_config()
+    rng = np.random.default_rng(11)
+    lens = rng.integers(1, 140000, 40)
+    lens[:6] = [1, 16384, 16385, 32768, 49153, 131072]
+    flat = rng.integers(0, cfg.p, int(lens.sum()), dtype=np.uint64)
+    plan = device.BatchPlan(cfg, lens)
+    d = device.to_words(flat, cfg)
+    want = O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K)
+    for _ in range(2):
+        plan.execute(d)
+        assert np.array_equal(device.from_words(d, cfg), want)
+        plan.execute(d, inverse=True)
+        assert np.array_equal(device.from_words(d, cfg), flat)
