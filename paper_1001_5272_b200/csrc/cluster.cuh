@@ -201,10 +201,7 @@ __global__ void __launch_bounds__(256, 3) k_cl_fwd(LaunchArgs<F> a) {
     const F f = a.f;
 
     const int64_t cbase = (int64_t)g * C;
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
-        const int64_t pos = cbase + i;
-        S[i + (i >> 5)] = pos < nin ? in[pos] : W(0);
-    }
+    tile_load<W>(S, in + cbase, nin - cbase, C, [](uint32_t, W w) { return w; });
     cl.sync();
 
     // cross stages: 2^gam-point untwisted column transforms over DSMEM
@@ -218,7 +215,7 @@ __global__ void __launch_bounds__(256, 3) k_cl_fwd(LaunchArgs<F> a) {
     fwd_rounds_ct<F, CL, CL>(f, S, TwDirect<F>{a.R.Zwf, g, CL, f});
 
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
-    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
+    tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
 }
 
 // column solve: rows j < M of column `ph` (physical index) hold the column's
@@ -285,10 +282,10 @@ __global__ void __launch_bounds__(256, 3) k_cl_inv(LaunchArgs<F> a) {
     const F f = a.f;
     const int64_t cbase = (int64_t)g * C;
 
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
-        const int64_t pos = cbase + i;
-        S[i + (i >> 5)] = pos < n ? load_pre(a, o + pos, x[pos]) : W(0);
-    }
+    if (a.pre)
+        tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
+    else
+        tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
     // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
     // known outputs [0, h), never the tail the columns will fill) alongside
@@ -318,5 +315,5 @@ __global__ void __launch_bounds__(256, 3) k_cl_inv(LaunchArgs<F> a) {
     }
     cl.sync();
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
-    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
+    tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
 }

@@ -88,10 +88,11 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             k_chunk_fwd<F><<<gchunk, kNT, sm_chunk, st>>>(a);
             g_launches += 2;
         } else {
-            k_chunk_inv<F><<<gchunk, kNT, sm_chunk, st>>>(a);
-            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
-            k_last_inv<F><<<glast, kNT, sm_last, st>>>(a);
-            k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
+            static const int stop = getenv("TFTB_DEBUG_STOP") ? atoi(getenv("TFTB_DEBUG_STOP")) : 9;  // debug knob
+            if (stop >= 1) k_chunk_inv<F><<<gchunk, kNT, sm_chunk, st>>>(a);
+            if (stop >= 2) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
+            if (stop >= 3) k_last_inv<F><<<glast, kNT, sm_last, st>>>(a);
+            if (stop >= 4) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
             g_launches += 4;
         }
         CK(cudaGetLastError());

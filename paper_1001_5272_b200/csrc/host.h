@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -130,6 +131,8 @@ int make_plan(int64_t n, Plan* pl) {
     }
     pl->kind = kLarge;
     int l0 = std::min(l / 2, Limits<F>::col_t - 4);
+    static const int force_l1 = getenv("TFTB_FORCE_L1") ? atoi(getenv("TFTB_FORCE_L1")) : 0;  // debug knob
+    if (force_l1 > 0 && force_l1 < l) l0 = l - force_l1;
     int l1 = l - l0;
     if (l1 > Limits<F>::chunk_max) {
         l1 = Limits<F>::chunk_max;
@@ -199,6 +202,8 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
                 const int64_t* h_len, PlanImpl* P);
 template <class F>
 int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st);
+
+int get_ring(uint64_t p, uint64_t top, int K, RingHost** out);  // tftb200.cu
 
 // defined per field in inst_f30.cu / inst_f32.cu / inst_f62.cu
 template <class F>

@@ -140,8 +140,7 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
     const uint32_t hs = MASK ? (uint32_t)(((uint64_t)h >> (s + 1)) << (s + 1)) : 0;
     const uint32_t hs1 = MASK ? (uint32_t)(((uint64_t)h >> (s + 2)) << (s + 2)) : 0;
     const bool scale_all = !MASK && s == last;
-    Tw<W> sc;
-    if (MASK || scale_all) sc = ipow2[s + 1];
+    const Tw<W> sc = ipow2[s + 1];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
 #pragma unroll

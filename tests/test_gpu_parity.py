@@ -199,3 +199,18 @@ def test_batch_plan_reuse_against_oracle():
         assert np.array_equal(device.from_words(d, cfg), want)
         plan.execute(d, inverse=True)
         assert np.array_equal(device.from_words(d, cfg), flat)
+
+
+def test_tile_plain_inverse_every_size():
+    """Regression: the unmasked in-tile inverse (two-pass chunk step) at every
+    tile size, through the internal debug entry point."""
+    import ctypes
+    cfg = T.default_config()
+    lib = backend.load()
+    f = lib.tftb_debug_intt_tile
+    f.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    for t in range(1, 15):
+        y = gen(t, cfg.p, 1 << t)
+        d = device.to_words(y, cfg)
+        backend.check(f(cfg.p, cfg.omegaK, cfg.K, d.data_ptr(), t))
+        assert np.array_equal(device.from_words(d, cfg), O.itft(y, cfg.p, cfg.omegaK, cfg.K)), t
