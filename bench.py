@@ -213,6 +213,9 @@ def main():
     from paper_1001_5272_b200 import backend, device
 
     torch.cuda.set_device(local)
+    if args.config != 2:
+        explore(args, T, device, backend, torch)
+        return
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -372,6 +375,73 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _time(fn, torch, reps, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def explore(args, T, device, backend, torch):
+    """Exploration lines for BASELINE configs 1, 3, 4, 5 (not the driver line)."""
+    peak, _ = peaks()
+    out = []
+    if args.config == 1:
+        cfg = T.default_config()
+        x = np.random.default_rng(0).integers(0, cfg.p, 1000, dtype=np.uint64)
+        d = device.to_words(x, cfg)
+        f = _time(lambda: device.tft_batch_(d, cfg, n=1000), torch, args.steps * 20)
+        i = _time(lambda: device.tft_batch_(d, cfg, n=1000, inverse=True), torch, args.steps * 20)
+        out.append({"config": 1, "n": 1000, "fwd_us": f * 1e3, "inv_us": i * 1e3})
+    elif args.config in (3, 5):
+        if args.config == 3:
+            cases = [(3221225473, n) for n in (1 << 24, (1 << 24) + 1, 3 << 23, (1 << 25) - 1, (1 << 25) + 1)]
+            cases += [(998244353, n) for n in (1 << 22, (1 << 22) + 1, 3 << 21, (1 << 23) - 1, 1 << 23)]
+        else:
+            ns = np.round(np.geomspace(1027, 268435451, 64)).astype(np.int64)
+            ns = [int(n) + 1 if n & (n - 1) == 0 else int(n) for n in ns]
+            cases = [(998244353 if n <= (1 << 23) else 3221225473, n) for n in ns]
+        for p, n in cases:
+            cfg = T.config_for_modulus(p) if p != 998244353 else T.default_config()
+            batch = max(1, (1 << 28) // n) if args.config == 5 else 1
+            w = 4 if p < (1 << 32) else 8
+            if batch * n * w > 6e9:
+                batch = max(1, int(6e9 // (n * w)))
+            d = torch.randint(0, 1 << 30, (batch * n,), dtype=torch.int32, device="cuda")
+            d.remainder_(p if p < (1 << 31) else (1 << 30))
+            plan = device.BatchPlan(cfg, np.full(batch, n))
+            f = _time(lambda: plan.execute(d), torch, args.steps)
+            i = _time(lambda: plan.execute(d, inverse=True), torch, args.steps)
+            byt = batch * 2 * passes_min(n, w) * n * w
+            out.append({"config": args.config, "p": p, "n": n, "batch": batch,
+                        "fwd_ms": f, "inv_ms": i,
+                        "fwd_gcoeff_s": batch * n / f / 1e6, "inv_gcoeff_s": batch * n / i / 1e6,
+                        "fwd_roofline_frac": byt / (f / 1e3) / 1e9 / peak,
+                        "inv_roofline_frac": byt / (i / 1e3) / 1e9 / peak})
+            del d, plan
+            torch.cuda.empty_cache()
+    elif args.config == 4:
+        cfg = T.default_config()
+        la, lb, pairs = 2500001, 1750004, 256
+        r = la + lb - 1
+        a = torch.randint(0, cfg.p, (pairs * la,), dtype=torch.int32, device="cuda")
+        b = torch.randint(0, cfg.p, (pairs * lb,), dtype=torch.int32, device="cuda")
+        x = torch.empty(pairs * r, dtype=torch.int32, device="cuda")
+        y = torch.empty(pairs * r, dtype=torch.int32, device="cuda")
+        t = _time(lambda: device.multiply_batch(a, b, x, cfg, pairs, la, lb, scratch=y), torch, args.steps, warm=1)
+        byt = pairs * (4 * (la + lb) + 3 * (2 * 2 * r * 4) + 3 * r * 4)
+        out.append({"config": 4, "pairs": pairs, "ms": t, "products_per_s": pairs / t * 1e3,
+                    "roofline_frac": byt / (t / 1e3) / 1e9 / peak})
+    for o in out:
+        print(json.dumps(o))
 
 
 if __name__ == "__main__":

@@ -68,6 +68,58 @@ struct TwDirect {
     }
 };
 
+// Twiddles for a tile that is block `blk` (64-bit) at level T of an arbitrarily
+// long transform: theta(s, J) = omega_{2 idx}, idx = blk 2^(T-s-1) + J.  Below
+// 2^zb the w-only table is read directly; above, idx = hi*2^zb + lo and
+// omega_{2 idx} = Zh[hi] * Z[lo] (product rule) costs one Montgomery product.
+// N-aligned runs of N <= 2^zb indices never straddle a 2^zb boundary.
+template <class F>
+struct TwBig {
+    const typename F::W* Zw;
+    const typename F::W* Zwh;
+    uint64_t blk;
+    int T, zb;
+    F f;
+    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
+        const uint64_t idx = (blk << (T - s - 1)) + J;
+        const uint64_t m = (1ull << zb) - 1;
+        if (idx <= m) return f.mk(__ldg(Zw + idx));
+        return f.mk(f.red1(f.mont(__ldg(Zwh + (idx >> zb)), __ldg(Zw + (idx & m)))));
+    }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
+        using W = typename F::W;
+        const uint64_t idx = (blk << (T - s - 1)) + J0;
+        const uint64_t m = (1ull << zb) - 1;
+        const W* p = Zw + (idx & m);
+        W lo[N];
+        constexpr int V = 16 / sizeof(W);
+        if constexpr (N >= V && V > 1) {
+#pragma unroll
+            for (int q = 0; q < N; q += V) {
+                if constexpr (sizeof(W) == 4) {
+                    uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
+                    lo[q] = t.x; lo[q + 1] = t.y; lo[q + 2] = t.z; lo[q + 3] = t.w;
+                } else {
+                    ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + q));
+                    lo[q] = t.x; lo[q + 1] = t.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < N; ++q) lo[q] = __ldg(p + q);
+        }
+        if (idx <= m) {
+#pragma unroll
+            for (int q = 0; q < N; ++q) out[q] = f.mk(lo[q]);
+        } else {
+            const W hi = __ldg(Zwh + (idx >> zb));
+#pragma unroll
+            for (int q = 0; q < N; ++q) out[q] = f.mk(f.red1(f.mont(hi, lo[q])));
+        }
+    }
+};
+
 // ------------------------------------------------------ compile-time rounds
 template <int SLO>
 struct PhysStep {
@@ -316,4 +368,79 @@ __global__ void __launch_bounds__(256, 3) k_cl_inv(LaunchArgs<F> a) {
     cl.sync();
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
+}
+
+// ================================================ two-pass plan, chunk pass
+// Chunks are 2^CL contiguous words = sub-block k of the network at level CL;
+// twiddles come from TwBig (block k).  grid: (max chunks, vectors).
+template <class F, int CL>
+__global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const uint32_t k = blockIdx.x;
+    const int64_t cbase = (int64_t)k * C;
+    if (cbase >= n) return;
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v) + cbase;
+    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    const int64_t avail = n - cbase;
+    tile_load<W>(S, x, avail, C, [&](uint32_t i, W w) { return (int64_t)i < avail ? w : st[i]; });
+    __syncthreads();
+    fwd_rounds_ct<F, CL, CL>(f, S, TwBig<F>{a.R.Zwf, a.R.Zwfh, k, CL, a.R.zb, f});
+    tile_store<W>(x, S, (uint32_t)min((int64_t)C, avail), [&](W w) { return f.canon(w); });
+}
+
+// step 1: complete chunks k < K.  grid: (max K, vectors)
+template <class F, int CL>
+__global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const uint32_t k = blockIdx.x;
+    if (k >= (uint64_t)(n >> CL)) return;
+    const F f = a.f;
+    const int64_t o = a.xd.o(v) + (int64_t)k * C;
+    W* x = a.x + o;
+    if (a.pre)
+        tile_load<W>(S, x, C, C, [&](uint32_t i, W w) { return load_pre(a, o + i, w); });
+    else
+        tile_load<W>(S, x, C, C, [](uint32_t, W w) { return w; });
+    __syncthreads();
+    inv_rounds_ct<F, CL, CL, false>(f, S, TwBig<F>{a.R.Zwi, a.R.Zwih, k, CL, a.R.zb, f}, a.R.ipow2);
+    tile_store<W>(x, S, C, [&](W w) { return f.canon(w); });
+}
+
+// step 3: the partial last chunk (h known outputs, C-h stashed inputs).
+// grid: (1, vectors)
+template <class F, int CL>
+__global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    if (!h) return;
+    const F f = a.f;
+    const int64_t o = a.xd.o(v) + (int64_t)K * C;
+    W* x = a.x + o;
+    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    if (a.pre)
+        tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? load_pre(a, o + i, w) : st[i]; });
+    else
+        tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? w : st[i]; });
+    __syncthreads();
+    const TwBig<F> tpf{a.R.Zwf, a.R.Zwfh, K, CL, a.R.zb, f}, tpi{a.R.Zwi, a.R.Zwih, K, CL, a.R.zb, f};
+    inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+    SmemTile<W> tl{S, CL, 0};
+    itft_phases23(f, tl, h, tpf, tpi, a.R);
+    tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });
 }

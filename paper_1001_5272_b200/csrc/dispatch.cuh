@@ -73,11 +73,11 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     Scratch stash;
     if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
     a.stash = stash_buf ? stash_buf : (W*)stash.p;
+    constexpr int CL = Limits<F>::CL;
     const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 64) * sizeof(W);
-    const size_t sm_chunk = (padded_words(C) + C + 64) * sizeof(W);
-    const size_t sm_last = (padded_words(C) + 2 * C + 64) * sizeof(W);
-    if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F>, sm_chunk) ||
-        set_smem(k_chunk_inv<F>, sm_chunk) || set_smem(k_last_inv<F>, sm_last))
+    const size_t sm_chunk = padded_words(C) * sizeof(W);
+    if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F, CL>, sm_chunk) ||
+        set_smem(k_chunk_inv<F, CL>, sm_chunk) || set_smem(k_last_inv<F, CL>, sm_chunk))
         return -1;
     for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
         a.vbase = v0;
@@ -85,13 +85,13 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
         if (!inverse) {
             k_col_fwd<F><<<gcol, kNT, sm_col, st>>>(a);
-            k_chunk_fwd<F><<<gchunk, kNT, sm_chunk, st>>>(a);
+            k_chunk_fwd<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
             g_launches += 2;
         } else {
             static const int stop = getenv("TFTB_DEBUG_STOP") ? atoi(getenv("TFTB_DEBUG_STOP")) : 9;  // debug knob
-            if (stop >= 1) k_chunk_inv<F><<<gchunk, kNT, sm_chunk, st>>>(a);
+            if (stop >= 1) k_chunk_inv<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
             if (stop >= 2) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
-            if (stop >= 3) k_last_inv<F><<<glast, kNT, sm_last, st>>>(a);
+            if (stop >= 3) k_last_inv<F, CL><<<glast, kNT, sm_chunk, st>>>(a);
             if (stop >= 4) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
             g_launches += 4;
         }

@@ -101,8 +101,7 @@ template <class F>
 struct Limits {
     // log2 words of one CTA's shared-memory chunk (64 KB) and of the column tiles
     static constexpr int CL = sizeof(typename F::W) == 4 ? 14 : 13;
-    static constexpr int col_t = sizeof(typename F::W) == 4 ? 13 : 12;
-    static constexpr int chunk_max = sizeof(typename F::W) == 4 ? 15 : 14;
+    static constexpr int col_t = sizeof(typename F::W) == 4 ? 14 : 13;
 };
 
 enum PlanKind { kSmall = 0, kCluster = 1, kLarge = 2 };
@@ -130,16 +129,12 @@ int make_plan(int64_t n, Plan* pl) {
         return 0;
     }
     pl->kind = kLarge;
-    int l0 = std::min(l / 2, Limits<F>::col_t - 4);
-    static const int force_l1 = getenv("TFTB_FORCE_L1") ? atoi(getenv("TFTB_FORCE_L1")) : 0;  // debug knob
-    if (force_l1 > 0 && force_l1 < l) l0 = l - force_l1;
-    int l1 = l - l0;
-    if (l1 > Limits<F>::chunk_max) {
-        l1 = Limits<F>::chunk_max;
-        l0 = l - l1;
-    }
-    int wlog = std::max(1, std::min(4, Limits<F>::col_t - l0));
-    if (l0 + wlog > Limits<F>::col_t + 1) return fail("transform length too large for the two-pass plan");
+    // chunks are one CTA's shared-memory tile (2^CL words); columns take the
+    // rest, as many adjacent columns per CTA as fit a 2^col_t-word tile
+    int l1 = CL;
+    int l0 = l - l1;
+    int wlog = std::max(0, std::min(4, Limits<F>::col_t - l0));
+    if (l0 + wlog > Limits<F>::col_t) return fail("transform length too large for the two-pass plan");
     pl->l0 = l0;
     pl->l1 = l1;
     pl->wlog = wlog;

@@ -214,65 +214,7 @@ __global__ void k_col_fwd(LaunchArgs<F> a) {
     }
 }
 
-// grid: (max chunks, vectors)
-template <class F>
-__global__ void k_chunk_fwd(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v);
-    const int l1 = a.l1;
-    const uint32_t C = 1u << l1, k = blockIdx.x;
-    if ((int64_t)k * C >= n) return;
-    const uint32_t K = (uint32_t)(n >> l1);
-    W* S = reinterpret_cast<W*>(smem_raw);
-    W* T = S + padded_words(C);
-    W* zeta = T + C;
-    W* x = a.x + a.xd.o(v) + (int64_t)k * C;
-    SmemTile<W> tl{S, l1, 0};
-    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x)
-        tl.at(i) = (k < K || (int64_t)k * C + i < n) ? x[i] : st[i];
-    if (k == 0) {
-        __syncthreads();
-        fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
-    } else {
-        build_heap(a.f, a.R, T, zeta, l1, k, false);
-        fwd_all(a.f, tl, TwHeap<F>{T, l1, a.f});
-    }
-    const uint32_t lim = k < K ? C : (uint32_t)(n - (int64_t)k * C);
-    for (uint32_t i = threadIdx.x; i < lim; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
-}
-
 // ------------------------------------------------------------ two-pass, inverse
-// step 1: complete chunks k < K.  grid: (max K, vectors)
-template <class F>
-__global__ void k_chunk_inv(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v);
-    const int l1 = a.l1;
-    const uint32_t C = 1u << l1, k = blockIdx.x;
-    const uint32_t K = (uint32_t)(n >> l1);
-    if (k >= K) return;
-    W* S = reinterpret_cast<W*>(smem_raw);
-    W* T = S + padded_words(C);
-    W* zeta = T + C;
-    const int64_t o = a.xd.o(v) + (int64_t)k * C;
-    W* x = a.x + o;
-    SmemTile<W> tl{S, l1, 0};
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) tl.at(i) = load_pre(a, o + i, x[i]);
-    if (k == 0) {
-        __syncthreads();
-        inv_all<F, false>(a.f, tl, TwPrefix<F>{a.R.Zi}, C, a.R.ipow2);
-    } else {
-        build_heap(a.f, a.R, T, zeta, l1, k, true);
-        inv_all<F, false>(a.f, tl, TwHeap<F>{T, l1, a.f}, C, a.R.ipow2);
-    }
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
-}
-
 // steps 2 (which = 0: columns c >= h, K rows, stash their row K) and
 // 4 (which = 1: columns c < h, K+1 rows).  grid: (C >> wlog, vectors)
 template <class F>
@@ -317,37 +259,6 @@ __global__ void k_col_inv(LaunchArgs<F> a, int which) {
             if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
         }
     }
-}
-
-// step 3: the partial last chunk.  grid: (1, vectors)
-template <class F>
-__global__ void k_last_inv(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v);
-    const int l1 = a.l1;
-    const uint32_t C = 1u << l1;
-    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
-    if (!h) return;
-    W* S = reinterpret_cast<W*>(smem_raw);
-    W* Tf = S + padded_words(C);
-    W* Ti = Tf + C;
-    W* zeta = Ti + C;
-    const int64_t o = a.xd.o(v) + (int64_t)K * C;
-    W* x = a.x + o;
-    const W* st = a.stash + (v - a.vbase) * (int64_t)C;
-    SmemTile<W> tl{S, l1, 0};
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) tl.at(i) = i < h ? load_pre(a, o + i, x[i]) : st[i];
-    if (K == 0) {
-        __syncthreads();
-        itft_gen(a.f, tl, h, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
-    } else {
-        build_heap(a.f, a.R, Tf, zeta, l1, K, false);
-        build_heap(a.f, a.R, Ti, zeta, l1, K, true);
-        itft_gen(a.f, tl, h, TwHeap<F>{Tf, l1, a.f}, TwHeap<F>{Ti, l1, a.f}, a.R);
-    }
-    for (uint32_t i = threadIdx.x; i < h; i += blockDim.x) x[i] = a.f.canon(tl.at(i));
 }
 
 // ------------------------------------------------------------ helpers

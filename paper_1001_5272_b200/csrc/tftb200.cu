@@ -120,15 +120,13 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
         }
     }
     size_t tw_bytes = host.size() * sizeof(Tw<W>);
-    CK(cudaMalloc(&rh->dmem, tw_bytes + 2 * nz * sizeof(W)));
+    const size_t nwords = 2 * nz + 2 * nh;
+    CK(cudaMalloc(&rh->dmem, tw_bytes + nwords * sizeof(W)));
     CK(cudaMemcpy(rh->dmem, host.data(), tw_bytes, cudaMemcpyHostToDevice));
-    std::vector<W> words(2 * nz);
-    for (size_t j = 0; j < nz; j++) {
-        words[j] = host[j].w;
-        words[nz + j] = host[nz + j].w;
-    }
+    std::vector<W> words(nwords);
+    for (size_t j = 0; j < nwords; j++) words[j] = host[j].w;  // zf, zi, zfh, zih in order
     W* dw = (W*)((char*)rh->dmem + tw_bytes);
-    CK(cudaMemcpy(dw, words.data(), 2 * nz * sizeof(W), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, words.data(), nwords * sizeof(W), cudaMemcpyHostToDevice));
     Tw<W>* d = (Tw<W>*)rh->dmem;
     out->Zf = d;
     out->Zi = d + nz;
@@ -138,6 +136,8 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     out->vinv = d + 2 * nz + 2 * nh + 64;
     out->Zwf = dw;
     out->Zwi = dw + nz;
+    out->Zwfh = dw + 2 * nz;
+    out->Zwih = dw + 2 * nz + nh;
     uint64_t R1 = tb.to_m(1);
     out->r2 = tb.tw(R1);  // Montgomery form of R is R^2 mod p
     out->inv2 = tb.tw(inv2);

@@ -41,6 +41,8 @@ struct RingDev {
     const Tw<W>* ipow2; // ipow2[k] = 2^-k, k < 64
     const W* Zwf;       // Montgomery words of Zf / Zi alone (companion recomputed
     const W* Zwi;       //   with one multiply: halves twiddle traffic)
+    const W* Zwfh;      // Montgomery words of Zfh / Zih
+    const W* Zwih;
     const Tw<W>* vinv;  // 8 blocks of 72: V_m^-1 (m x m, V_m[s][i] = omega_s^i), then omega_m^i
 
     Tw<W> r2;           // R^2 mod p (Montgomery form of R): mont(x, r2.w) = x R
