@@ -394,7 +394,10 @@ __global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
     tile_store<W>(x, S, (uint32_t)min((int64_t)C, avail), [&](W w) { return f.canon(w); });
 }
 
-// step 1: complete chunks k < K.  grid: (max K, vectors)
+// step 1: complete chunks k < K, plus phase 1 of the partial chunk K (the
+// masked inverse of the complete binary blocks of its h known outputs, which
+// needs nothing from the columns) so the serial step 3 only runs the two
+// O(2^CL) sweeps.  grid: (max chunks, vectors)
 template <class F, int CL>
 __global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
     using W = typename F::W;
@@ -404,21 +407,25 @@ __global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
     const int64_t v = a.vbase + blockIdx.y;
     const int64_t n = a.xd.n(v);
     const uint32_t k = blockIdx.x;
-    if (k >= (uint64_t)(n >> CL)) return;
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    if (k > K || (k == K && !h)) return;
+    const uint32_t len = k < K ? C : h;
     const F f = a.f;
     const int64_t o = a.xd.o(v) + (int64_t)k * C;
     W* x = a.x + o;
     if (a.pre)
-        tile_load<W>(S, x, C, C, [&](uint32_t i, W w) { return load_pre(a, o + i, w); });
+        tile_load<W>(S, x, len, C, [&](uint32_t i, W w) { return load_pre(a, o + i, w); });
     else
-        tile_load<W>(S, x, C, C, [](uint32_t, W w) { return w; });
+        tile_load<W>(S, x, len, C, [](uint32_t, W w) { return w; });
     __syncthreads();
-    inv_rounds_ct<F, CL, CL, false>(f, S, TwBig<F>{a.R.Zwi, a.R.Zwih, k, CL, a.R.zb, f}, a.R.ipow2);
-    tile_store<W>(x, S, C, [&](W w) { return f.canon(w); });
+    const TwBig<F> tpi{a.R.Zwi, a.R.Zwih, k, CL, a.R.zb, f};
+    if (k < K) inv_rounds_ct<F, CL, CL, false>(f, S, tpi, a.R.ipow2);
+    else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+    tile_store<W>(x, S, len, [&](W w) { return f.canon(w); });
 }
 
-// step 3: the partial last chunk (h known outputs, C-h stashed inputs).
-// grid: (1, vectors)
+// step 3: the partial last chunk: its h slots already hold the phase-1
+// values (k_chunk_inv); the C-h stashed inputs complete it.  grid: (1, vectors)
 template <class F, int CL>
 __global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
     using W = typename F::W;
@@ -433,13 +440,9 @@ __global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
     const int64_t o = a.xd.o(v) + (int64_t)K * C;
     W* x = a.x + o;
     const W* st = a.stash + (v - a.vbase) * (int64_t)C;
-    if (a.pre)
-        tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? load_pre(a, o + i, w) : st[i]; });
-    else
-        tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? w : st[i]; });
+    tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? w : st[i]; });
     __syncthreads();
     const TwBig<F> tpf{a.R.Zwf, a.R.Zwfh, K, CL, a.R.zb, f}, tpi{a.R.Zwi, a.R.Zwih, K, CL, a.R.zb, f};
-    inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
     SmemTile<W> tl{S, CL, 0};
     itft_phases23(f, tl, h, tpf, tpi, a.R);
     tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });
