@@ -217,28 +217,43 @@ TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint
     for (int j = 0; j < GP / 2; ++j) tw[j] = f.mk(__ldg(Zw + j));
     uint32_t lo, hi;
     col_share(0, C, g, G, lo, hi);
-    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
-        const uint32_t ph = c + (c >> 5);
-        W col[GP];
+    // UNR columns per thread in flight: DSMEM loads are ~200+ cycles each
+    constexpr int UNR = GP <= 2 ? 8 : (GP <= 4 ? 4 : 2);
+    for (uint32_t c0 = lo + threadIdx.x; c0 < hi; c0 += blockDim.x * UNR) {
+        W col[UNR][GP];
 #pragma unroll
-        for (int j = 0; j < GP; ++j) col[j] = j < (int)G ? rs[j][ph] : W(0);
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t c = c0 + u * blockDim.x;
+            const uint32_t ph = c + (c >> 5);
 #pragma unroll
-        for (int sp = GAM - 1; sp >= 0; --sp) {
+            for (int j = 0; j < GP; ++j) col[u][j] = (j < (int)G && c < hi) ? rs[j][ph] : W(0);
+        }
 #pragma unroll
-            for (int j = 0; j < GP; ++j) {
-                if ((j >> sp) & 1) continue;
-                f.fwd(col[j], col[j + (1 << sp)], tw[j >> (sp + 1)]);
+        for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+            for (int sp = GAM - 1; sp >= 0; --sp) {
+#pragma unroll
+                for (int j = 0; j < GP; ++j) {
+                    if ((j >> sp) & 1) continue;
+                    f.fwd(col[u][j], col[u][j + (1 << sp)], tw[j >> (sp + 1)]);
+                }
             }
         }
 #pragma unroll
-        for (int j = 0; j < GP; ++j)
-            if (j < (int)G) rs[j][ph] = col[j];
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t c = c0 + u * blockDim.x;
+            if (c >= hi) break;
+            const uint32_t ph = c + (c >> 5);
+#pragma unroll
+            for (int j = 0; j < GP; ++j)
+                if (j < (int)G) rs[j][ph] = col[u][j];
+        }
     }
 }
 
 // ------------------------------------------------------------ kernels
-template <class F, int CL>
-__global__ void __launch_bounds__(256, 3) k_cl_fwd(LaunchArgs<F> a) {
+template <class F, int CL, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_cl_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -274,12 +289,12 @@ __global__ void __launch_bounds__(256, 3) k_cl_fwd(LaunchArgs<F> a) {
 // first M outputs; replace them by its M coefficients (V_M^-1, M^2 products);
 // optionally write the next output sum_j x_j omega_M^j into row M.
 template <class F, int M>
-TFT_DEV void col_solve_m(const F& f, typename F::W* const* rs, uint32_t ph, const Tw<typename F::W>* blk,
-                         bool write_next) {
+TFT_DEV void col_solve_vals(const F& f, typename F::W* const* rs, uint32_t ph, const typename F::W* yin,
+                            const Tw<typename F::W>* blk, bool write_next) {
     using W = typename F::W;
     W y[M], xv[M];
 #pragma unroll
-    for (int j = 0; j < M; ++j) y[j] = f.canon(rs[j][ph]);
+    for (int j = 0; j < M; ++j) y[j] = f.canon(yin[j]);
 #pragma unroll
     for (int r = 0; r < M; ++r) {
         W acc = 0;
@@ -300,7 +315,14 @@ TFT_DEV void col_solve_m(const F& f, typename F::W* const* rs, uint32_t ph, cons
 template <class F, int M>
 TFT_DEV void col_solve_range(const F& f, typename F::W* const* rs, uint32_t lo, uint32_t hi,
                              const Tw<typename F::W>* blk, bool write_next) {
-    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) col_solve_m<F, M>(f, rs, c + (c >> 5), blk, write_next);
+    using W = typename F::W;
+    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+        const uint32_t ph = c + (c >> 5);
+        W y[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) y[j] = rs[j][ph];
+        col_solve_vals<F, M>(f, rs, ph, y, blk, write_next);
+    }
 }
 
 template <class F>
@@ -318,8 +340,8 @@ TFT_DEV void col_solve(const F& f, typename F::W* const* rs, uint32_t lo, uint32
     }
 }
 
-template <class F, int CL>
-__global__ void __launch_bounds__(256, 3) k_cl_inv(LaunchArgs<F> a) {
+template <class F, int CL, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);

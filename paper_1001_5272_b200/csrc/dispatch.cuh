@@ -27,7 +27,10 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     if (pl.kind == kCluster) {
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
-        if (set_smem(k_cl_fwd<F, CL>, smem) || set_smem(k_cl_inv<F, CL>, smem)) return -1;
+        static const int minb = getenv("TFTB_CL_MINB") ? atoi(getenv("TFTB_CL_MINB")) : 3;  // tuning knob
+        auto kf = minb == 2 ? k_cl_fwd<F, CL, 2> : k_cl_fwd<F, CL, 3>;
+        auto ki = minb == 2 ? k_cl_inv<F, CL, 2> : k_cl_inv<F, CL, 3>;
+        if (set_smem(kf, smem) || set_smem(ki, smem)) return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
@@ -43,8 +46,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (inverse) CK(cudaLaunchKernelEx(&lc, k_cl_inv<F, CL>, a));
-            else CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F, CL>, a));
+            if (inverse) CK(cudaLaunchKernelEx(&lc, ki, a));
+            else CK(cudaLaunchKernelEx(&lc, kf, a));
             g_launches++;
         }
         return 0;

@@ -29,8 +29,11 @@ def launches(path):
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[start]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    mi = h.index("Metric Name")
     agg = OrderedDict()
     for r in rows[start + 1:]:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
         name = r[ki].split("(")[0]
         agg.setdefault(name, []).append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
