@@ -28,94 +28,78 @@
 
 namespace cg = cooperative_groups;
 
+// read-only load of one twiddle pair
+template <typename W>
+TFT_DEV Tw<W> ldg_tw(const Tw<W>* p) {
+    if constexpr (sizeof(W) == 4) {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        return Tw<W>{t.x, t.y};
+    } else {
+        const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p));
+        return Tw<W>{t.x, t.y};
+    }
+}
+
+// N consecutive twiddle pairs from an N-aligned index (true for every call in
+// reg_fwd / reg_inv), 16-byte loads
+template <typename W, int N>
+TFT_DEV void ldg_tw_run(const Tw<W>* p, Tw<W>* out) {
+    if constexpr (sizeof(W) == 4 && N >= 2) {
+#pragma unroll
+        for (int q = 0; q < N; q += 2) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
+            out[q] = Tw<W>{t.x, t.y};
+            out[q + 1] = Tw<W>{t.z, t.w};
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) out[q] = ldg_tw(p + q);
+    }
+}
+
 // Direct twiddles for a tile that is block `blk` at level T:
-// theta(s, J) = omega_{2 (blk 2^(T-s-1) + J)} read from the w-only table.
+// theta(s, J) = omega_{2 (blk 2^(T-s-1) + J)} from the 2^zb-entry table.
 template <class F>
 struct TwDirect {
-    const typename F::W* Zw;
+    const Tw<typename F::W>* Z;
     uint32_t blk;
     int T;
     F f;
-    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
-        return f.mk(__ldg(Zw + ((blk << (T - s - 1)) + J)));
-    }
-    // N consecutive twiddles from an N-aligned index (true for every call in
-    // reg_fwd / reg_inv), with 16-byte loads where the word type allows
+    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const { return ldg_tw(Z + ((blk << (T - s - 1)) + J)); }
     template <int N>
     TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
-        using W = typename F::W;
-        const W* p = Zw + ((blk << (T - s - 1)) + J0);
-        constexpr int V = 16 / sizeof(W);
-        if constexpr (N >= V && V > 1) {
-#pragma unroll
-            for (int q = 0; q < N; q += V) {
-                if constexpr (sizeof(W) == 4) {
-                    uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
-                    out[q] = f.mk(t.x);
-                    out[q + 1] = f.mk(t.y);
-                    out[q + 2] = f.mk(t.z);
-                    out[q + 3] = f.mk(t.w);
-                } else {
-                    ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + q));
-                    out[q] = f.mk(t.x);
-                    out[q + 1] = f.mk(t.y);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < N; ++q) out[q] = f.mk(__ldg(p + q));
-        }
+        ldg_tw_run<typename F::W, N>(Z + ((blk << (T - s - 1)) + J0), out);
     }
 };
 
 // Twiddles for a tile that is block `blk` (64-bit) at level T of an arbitrarily
 // long transform: theta(s, J) = omega_{2 idx}, idx = blk 2^(T-s-1) + J.  Below
-// 2^zb the w-only table is read directly; above, idx = hi*2^zb + lo and
-// omega_{2 idx} = Zh[hi] * Z[lo] (product rule) costs one Montgomery product.
-// N-aligned runs of N <= 2^zb indices never straddle a 2^zb boundary.
+// 2^zb the table is read directly; above, idx = hi*2^zb + lo and
+// omega_{2 idx} = Zh[hi] * Z[lo] (product rule) costs one twiddle product and
+// one companion.  N-aligned runs of N <= 2^zb indices never straddle a 2^zb
+// boundary.
 template <class F>
 struct TwBig {
-    const typename F::W* Zw;
-    const typename F::W* Zwh;
+    const Tw<typename F::W>* Z;
+    const Tw<typename F::W>* Zh;
     uint64_t blk;
     int T, zb;
     F f;
     TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
         const uint64_t idx = (blk << (T - s - 1)) + J;
         const uint64_t m = (1ull << zb) - 1;
-        if (idx <= m) return f.mk(__ldg(Zw + idx));
-        return f.mk(f.red1(f.mont(__ldg(Zwh + (idx >> zb)), __ldg(Zw + (idx & m)))));
+        if (idx <= m) return ldg_tw(Z + idx);
+        return f.tw(f.twmul(ldg_tw(Zh + (idx >> zb)), ldg_tw(Z + (idx & m))));
     }
     template <int N>
     TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
-        using W = typename F::W;
         const uint64_t idx = (blk << (T - s - 1)) + J0;
         const uint64_t m = (1ull << zb) - 1;
-        const W* p = Zw + (idx & m);
-        W lo[N];
-        constexpr int V = 16 / sizeof(W);
-        if constexpr (N >= V && V > 1) {
+        ldg_tw_run<typename F::W, N>(Z + (idx & m), out);
+        if (idx > m) {
+            const Tw<typename F::W> hi = ldg_tw(Zh + (idx >> zb));
 #pragma unroll
-            for (int q = 0; q < N; q += V) {
-                if constexpr (sizeof(W) == 4) {
-                    uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
-                    lo[q] = t.x; lo[q + 1] = t.y; lo[q + 2] = t.z; lo[q + 3] = t.w;
-                } else {
-                    ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p + q));
-                    lo[q] = t.x; lo[q + 1] = t.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < N; ++q) lo[q] = __ldg(p + q);
-        }
-        if (idx <= m) {
-#pragma unroll
-            for (int q = 0; q < N; ++q) out[q] = f.mk(lo[q]);
-        } else {
-            const W hi = __ldg(Zwh + (idx >> zb));
-#pragma unroll
-            for (int q = 0; q < N; ++q) out[q] = f.mk(f.red1(f.mont(hi, lo[q])));
+            for (int q = 0; q < N; ++q) out[q] = f.tw(f.twmul(hi, out[q]));
         }
     }
 };
@@ -144,7 +128,7 @@ TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp) {
 }
 
 // unmasked inverse round; the tile's last stage (s = TL-1) also scales by 2^-TL
-template <class F, int TL, int KK, int SLO, bool MASK, class TP>
+template <class F, int TL, int KK, int SLO, bool MASK, class TP, bool SCALE = true>
 TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
                           uint32_t h) {
     using W = typename F::W;
@@ -158,7 +142,7 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
         W v[1 << KK];
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
-        reg_inv<F, KK, 0, MASK>(f, v, base, SLO, tp, h, TL - 1, ipow2);
+        reg_inv<F, KK, 0, MASK>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
     }
@@ -179,16 +163,16 @@ TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp) {
     }
 }
 
-template <class F, int TL, int SHI, bool MASK, class TP>
+template <class F, int TL, int SHI, bool MASK, class TP, bool SCALE = true>
 TFT_DEV void inv_rounds_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
                            uint32_t h = 0) {
     if constexpr (SHI <= 5) {
-        inv_round_ct<F, TL, SHI, 0, MASK>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, SHI, 0, MASK, TP, SCALE>(f, S, tp, ipow2, h);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        inv_rounds_ct<F, TL, SHI - KK, MASK>(f, S, tp, ipow2, h);
-        inv_round_ct<F, TL, KK, SHI - KK, MASK>(f, S, tp, ipow2, h);
+        inv_rounds_ct<F, TL, SHI - KK, MASK, TP, SCALE>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, KK, SHI - KK, MASK, TP, SCALE>(f, S, tp, ipow2, h);
         __syncthreads();
     }
 }
@@ -206,7 +190,7 @@ __device__ __forceinline__ void col_share(uint32_t c0, uint32_t C, uint32_t g, u
 // rows j >= G are past n (zero in, dropped out)
 template <class F, int GAM>
 TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint32_t g, uint32_t G, uint32_t C,
-                       const typename F::W* Zw) {
+                       const Tw<typename F::W>* Zw) {
     using W = typename F::W;
     constexpr int GP = 1 << GAM;
     W* rs[GP];
@@ -214,7 +198,7 @@ TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint
     for (int j = 0; j < GP; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
     Tw<W> tw[GP / 2 > 0 ? GP / 2 : 1];
 #pragma unroll
-    for (int j = 0; j < GP / 2; ++j) tw[j] = f.mk(__ldg(Zw + j));
+    for (int j = 0; j < GP / 2; ++j) tw[j] = ldg_tw(Zw + j);
     uint32_t lo, hi;
     col_share(0, C, g, G, lo, hi);
     // UNR columns per thread in flight: DSMEM loads are ~200+ cycles each
@@ -252,8 +236,8 @@ TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint
 }
 
 // ------------------------------------------------------------ kernels
-template <class F, int CL, int MINB = 3>
-__global__ void __launch_bounds__(256, MINB) k_cl_fwd(LaunchArgs<F> a) {
+template <class F, int CL, int MINB = 3, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -273,13 +257,13 @@ __global__ void __launch_bounds__(256, MINB) k_cl_fwd(LaunchArgs<F> a) {
 
     // cross stages: 2^gam-point untwisted column transforms over DSMEM
     switch (gam) {
-        case 1: cross_fwd<F, 1>(f, cl, S, g, G, C, a.R.Zwf); break;
-        case 2: cross_fwd<F, 2>(f, cl, S, g, G, C, a.R.Zwf); break;
-        default: cross_fwd<F, 3>(f, cl, S, g, G, C, a.R.Zwf); break;
+        case 1: cross_fwd<F, 1>(f, cl, S, g, G, C, a.R.Zf); break;
+        case 2: cross_fwd<F, 2>(f, cl, S, g, G, C, a.R.Zf); break;
+        default: cross_fwd<F, 3>(f, cl, S, g, G, C, a.R.Zf); break;
     }
     cl.sync();
 
-    fwd_rounds_ct<F, CL, CL>(f, S, TwDirect<F>{a.R.Zwf, g, CL, f});
+    fwd_rounds_ct<F, CL, CL>(f, S, TwDirect<F>{a.R.Zf, g, CL, f});
 
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
@@ -340,8 +324,8 @@ TFT_DEV void col_solve(const F& f, typename F::W* const* rs, uint32_t lo, uint32
     }
 }
 
-template <class F, int CL, int MINB = 3>
-__global__ void __launch_bounds__(256, MINB) k_cl_inv(LaunchArgs<F> a) {
+template <class F, int CL, int MINB = 3, int NT = 256>
+__global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -363,8 +347,9 @@ __global__ void __launch_bounds__(256, MINB) k_cl_inv(LaunchArgs<F> a) {
     __syncthreads();
     // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
     // known outputs [0, h), never the tail the columns will fill) alongside
-    const TwDirect<F> tpi{a.R.Zwi, g, CL, f};
-    if (g < K) inv_rounds_ct<F, CL, CL, false>(f, S, tpi, a.R.ipow2);
+    const TwDirect<F> tpi{a.R.Zi, g, CL, f};
+    // complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
+    if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
     cl.sync();
 
@@ -374,22 +359,26 @@ __global__ void __launch_bounds__(256, MINB) k_cl_inv(LaunchArgs<F> a) {
     {
         uint32_t lo, hi;
         col_share(h, C, g, G, lo, hi);
-        col_solve(f, rs, lo, hi, (int)K, a.R.vinv + 72 * (K - 1), h != 0);
+        col_solve(f, rs, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1), h != 0);
     }
     cl.sync();
+    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     if (h && g == K) {
         SmemTile<W> tl{S, CL, 0};
-        itft_phases23(f, tl, h, TwDirect<F>{a.R.Zwf, K, CL, f}, tpi, a.R);
+        itft_phases23(f, tl, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
+    } else if (h) {
+        // columns >= h of this chunk are final: store them while chunk K is solved
+        for (uint32_t i = h + threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
     }
     cl.sync();
     if (h) {
         uint32_t lo, hi;
         col_share(0, h, g, G, lo, hi);
-        col_solve(f, rs, lo, hi, (int)K + 1, a.R.vinv + 72 * K, false);
+        col_solve(f, rs, lo, hi, (int)K + 1, a.R.vinvT + 72 * K, false);
     }
     cl.sync();
-    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
-    tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
+    if (!h || g == K) tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
+    else tile_store<W>(x + cbase, S, h, [&](W w) { return f.canon(w); });
 }
 
 // ================================================ two-pass plan, chunk pass
@@ -412,7 +401,7 @@ __global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
     const int64_t avail = n - cbase;
     tile_load<W>(S, x, avail, C, [&](uint32_t i, W w) { return (int64_t)i < avail ? w : st[i]; });
     __syncthreads();
-    fwd_rounds_ct<F, CL, CL>(f, S, TwBig<F>{a.R.Zwf, a.R.Zwfh, k, CL, a.R.zb, f});
+    fwd_rounds_ct<F, CL, CL>(f, S, TwBig<F>{a.R.Zf, a.R.Zfh, k, CL, a.R.zb, f});
     tile_store<W>(x, S, (uint32_t)min((int64_t)C, avail), [&](W w) { return f.canon(w); });
 }
 
@@ -440,7 +429,7 @@ __global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
     else
         tile_load<W>(S, x, len, C, [](uint32_t, W w) { return w; });
     __syncthreads();
-    const TwBig<F> tpi{a.R.Zwi, a.R.Zwih, k, CL, a.R.zb, f};
+    const TwBig<F> tpi{a.R.Zi, a.R.Zih, k, CL, a.R.zb, f};
     if (k < K) inv_rounds_ct<F, CL, CL, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
     tile_store<W>(x, S, len, [&](W w) { return f.canon(w); });
@@ -464,7 +453,7 @@ __global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
     const W* st = a.stash + (v - a.vbase) * (int64_t)C;
     tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? w : st[i]; });
     __syncthreads();
-    const TwBig<F> tpf{a.R.Zwf, a.R.Zwfh, K, CL, a.R.zb, f}, tpi{a.R.Zwi, a.R.Zwih, K, CL, a.R.zb, f};
+    const TwBig<F> tpf{a.R.Zf, a.R.Zfh, K, CL, a.R.zb, f}, tpi{a.R.Zi, a.R.Zih, K, CL, a.R.zb, f};
     SmemTile<W> tl{S, CL, 0};
     itft_phases23(f, tl, h, tpf, tpi, a.R);
     tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });

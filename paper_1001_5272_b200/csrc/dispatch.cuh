@@ -28,15 +28,16 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
         static const int minb = getenv("TFTB_CL_MINB") ? atoi(getenv("TFTB_CL_MINB")) : 3;  // tuning knob
-        auto kf = minb == 2 ? k_cl_fwd<F, CL, 2> : k_cl_fwd<F, CL, 3>;
-        auto ki = minb == 2 ? k_cl_inv<F, CL, 2> : k_cl_inv<F, CL, 3>;
+        const int nt = minb == 4 ? 512 : 256;  // 4 -> 512-thread CTAs, 2 per SM
+        auto kf = minb == 2 ? k_cl_fwd<F, CL, 2> : (minb == 4 ? k_cl_fwd<F, CL, 2, 512> : k_cl_fwd<F, CL, 3>);
+        auto ki = minb == 2 ? k_cl_inv<F, CL, 2> : (minb == 4 ? k_cl_inv<F, CL, 2, 512> : k_cl_inv<F, CL, 3>);
         if (set_smem(kf, smem) || set_smem(ki, smem)) return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3(pl.G, nv, 1);
-            lc.blockDim = dim3(kNT, 1, 1);
+            lc.blockDim = dim3(nt, 1, 1);
             lc.dynamicSmemBytes = smem;
             lc.stream = st;
             cudaLaunchAttribute at[1];

@@ -8,14 +8,18 @@
 //   F62 — odd p < 2^62 (the reference's modulus bound, modring.py:88-89),
 //         uint64 words, Harvey lazy butterflies (4p < 2^64).
 //
-// Twiddles are stored in Montgomery form wM = w*R mod p (R = 2^32 or 2^64)
-// together with a companion wMp = wM * (+-p^-1) mod R, so b*w mod p costs
-// three integer multiplies and no division (Montgomery reduction with the
-// quotient digit m = lo(b*wM) * (+-p^-1) = b*wMp precomputed per twiddle):
-//   F30:      m = b*wMp, r = (b*wM + m*p) >> 32          (companion -p^-1)
-//   F32/F62:  m = b*wMp, r = hi(b*wM) - hi(m*p) (+p)      (companion +p^-1)
-// both exact because the low words cancel.  Results lie in [0, 2p); F32
-// folds back to [0, p).
+// Twiddle multiplication b*w mod p costs three integer multiplies and no
+// division, with a per-twiddle companion stored next to w (Tw<W>):
+//   F30:      Shoup.  w in normal form, ws = floor(w 2^32 / p);
+//             q = hi(b ws), r = b w - q p in [0, 2p) for any 32-bit b.
+//             (IMAD.HI + 2 IMAD = 4 FMA-pipe slots on sm_100a; IMAD.HI and
+//             IMAD.WIDE issue at half rate, measured, so this beats REDC.)
+//   F32/F62:  Montgomery.  wM = w R mod p, companion wM p^-1 mod R;
+//             m = b*wMp, r = hi(b wM) - hi(m p) (+p).
+// "Field words" are the stored form (normal for F30, Montgomery for F32/F62);
+// tw(x) builds a full twiddle from a canonical field word and twmul multiplies
+// two twiddles into a field word.  mont(a, b) = a b R^-1 is the
+// representation-free product used for data x data (the pointwise product).
 // Reference: the scalar `(u128)a*b % p` of `_kernels.pyx:17-18`.
 #pragma once
 #include <cstdint>
@@ -31,27 +35,28 @@ struct Tw {
 struct F30 {
     using W = uint32_t;
     static constexpr bool kLazy = true;
-    W p, p2, pinv;  // pinv holds -p^-1 mod 2^32 for this field (REDC sign)
+    W p, p2, pinv;  // pinv = p^-1 mod 2^32
+    W npinv;        // -p^-1 mod 2^32 (REDC)
+    W c32, c32s;    // 2^32 mod p as a Shoup twiddle (companion generation)
 
     TFT_DEV W red2(W x) const { return min(x, x - p2); }  // [0,4p) -> [0,2p)
     TFT_DEV W red1(W x) const { return min(x, x - p); }   // [0,2p) -> [0,p)
     TFT_DEV W canon(W x) const { return red1(red2(x)); }
-    // b * w for any b < 4p: REDC of T = b*wM with m = b*wMp = lo(T)*(-p^-1):
-    // (T + m p) / 2^32 in [0, 2p).  Written as one 64-bit sum so ptxas emits
-    // IMAD, IMAD.WIDE and one IMAD.HI with the 64-bit addend (no negations).
-    TFT_DEV W mulw(W b, W wM, W wMp) const {
-        const uint32_t m = b * wMp;
-        const uint64_t t = (uint64_t)b * wM + (uint64_t)m * p;
-        return (W)(t >> 32);
-    }
+    // Shoup: b * w for any 32-bit b, result in [0, 2p)
+    TFT_DEV W mulw(W b, W w, W ws) const { return b * w - __umulhi(b, ws) * p; }
     TFT_DEV W mulw(W b, Tw<W> t) const { return mulw(b, t.w, t.wp); }
-    // Montgomery product a*b/R for a, b < 2p: [0, 2p)
+    // Shoup companion of a canonical w: w 2^32 = ws p + r, so ws = -r p^-1 mod 2^32
+    TFT_DEV Tw<W> tw(W w) const {
+        const W r = red1(mulw(w, c32, c32s));
+        return Tw<W>{w, (0u - r) * pinv};
+    }
+    TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return red1(mulw(a.w, b)); }
+    // REDC a*b/2^32 for a*b < p 2^32: [0, 2p)
     TFT_DEV W mont(W a, W b) const {
         const uint64_t ab = (uint64_t)a * b;
-        const uint32_t m = (uint32_t)ab * pinv;
+        const uint32_t m = (uint32_t)ab * npinv;
         return (W)((ab + (uint64_t)m * p) >> 32);
     }
-    TFT_DEV Tw<W> mk(W wM) const { return Tw<W>{wM, wM * pinv}; }
     // Cooley-Tukey (DIT on the remainder tree) butterfly: (a + w b, a - w b).
     // in [0,4p) -> out [0,4p)
     TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
@@ -67,7 +72,6 @@ struct F30 {
         x = s;
         y = mulw(d, t);
     }
-    TFT_DEV W lazy_in(W x) const { return x; }  // canonical input is a valid lazy value
     // canonical-in/canonical-out helpers (cheap paths of the inverse solver)
     TFT_DEV W cadd(W a, W b) const { return red1(a + b); }
     TFT_DEV W csub(W a, W b) const { return red1(a - b + p); }
@@ -97,7 +101,8 @@ struct F32 {
         W d = hi - u;
         return hi < u ? d + p : d;
     }
-    TFT_DEV Tw<W> mk(W wM) const { return Tw<W>{wM, wM * pinv}; }
+    TFT_DEV Tw<W> tw(W wM) const { return Tw<W>{wM, wM * pinv}; }
+    TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return mont(a.w, b.w); }
     TFT_DEV W cadd(W a, W b) const {
         W s = a + b;
         return (s < a || s >= p) ? s - p : s;
@@ -119,7 +124,6 @@ struct F32 {
         x = s;
         y = mulw(d, t);
     }
-    TFT_DEV W lazy_in(W x) const { return x; }
 };
 
 struct F62 {
@@ -141,7 +145,8 @@ struct F62 {
         W m = a * b * pinv;
         return hi - __umul64hi(m, p) + p;
     }
-    TFT_DEV Tw<W> mk(W wM) const { return Tw<W>{wM, wM * pinv}; }
+    TFT_DEV Tw<W> tw(W wM) const { return Tw<W>{wM, wM * pinv}; }
+    TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return red1(mont(a.w, b.w)); }
     TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
         W a = red2(x);
         W b = mulw(y, t);
@@ -154,7 +159,6 @@ struct F62 {
         x = s;
         y = mulw(d, t);
     }
-    TFT_DEV W lazy_in(W x) const { return x; }
     TFT_DEV W cadd(W a, W b) const { return red1(a + b); }
     TFT_DEV W csub(W a, W b) const { return red1(a - b + p); }
     TFT_DEV W cmulw(W b, Tw<W> t) const { return red1(mulw(b, t)); }

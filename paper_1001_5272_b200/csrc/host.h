@@ -81,7 +81,11 @@ F make_field(uint64_t p) {
     f.p = (typename F::W)p;
     f.p2 = (typename F::W)(2 * p);
     f.pinv = inv_word<typename F::W>((typename F::W)p);
-    if (std::is_same<F, F30>::value) f.pinv = (typename F::W)(0u - f.pinv);  // F30 uses the REDC sign
+    if constexpr (std::is_same<F, F30>::value) {
+        f.npinv = (uint32_t)(0u - f.pinv);
+        f.c32 = (uint32_t)(((unsigned __int128)1 << 32) % p);
+        f.c32s = (uint32_t)(((unsigned __int128)f.c32 << 32) / p);
+    }
     return f;
 }
 

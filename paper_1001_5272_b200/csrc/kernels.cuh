@@ -53,7 +53,7 @@ template <class F>
 TFT_DEV typename F::W load_pre(const LaunchArgs<F>& a, int64_t idx, typename F::W v) {
     if (!a.pre) return v;
     // X^ * Y^ : Montgomery product then * R^2 to undo the R^-1.
-    return a.f.canon(a.f.mont(a.f.red1(a.f.mont(v, a.pre[idx])), a.R.r2.w));
+    return a.f.canon(a.f.mont(a.f.red1(a.f.mont(v, a.pre[idx])), a.R.r2w));
 }
 
 // ------------------------------------------------------ tile <-> HBM streaming
@@ -253,7 +253,7 @@ __global__ void k_col_inv(LaunchArgs<F> a, int which) {
     }
     if (which == 0 && h) {
         // the column's first virtual output z_c[K] = sum_{i<K} x_i omega_K^i
-        colsum_pow(a.f, tl, K, omega_m(a.f, a.R, K), a.R.oneM, red, nv);
+        colsum_pow(a.f, tl, K, omega_w(a.f, a.R, K), a.R.oneW, red, nv);
         for (uint32_t col = threadIdx.x; col < ncols; col += blockDim.x) {
             uint32_t c = c0 + col;
             if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];

@@ -27,9 +27,10 @@ struct TableBuilder {
     uint64_t p;
     int bits;
     W pinv;
-    uint64_t R1;  // R mod p
+    bool shoup;   // F30: {w, floor(w 2^32 / p)}; else Montgomery {wR, wR p^-1}
     uint64_t to_m(uint64_t w) const { return (uint64_t)(((u128)w << bits) % p); }
     Tw<W> tw(uint64_t w) const {
+        if (shoup) return Tw<W>{(W)w, (W)(((u128)w << 32) / p)};
         W wm = (W)to_m(w);
         return Tw<W>{wm, (W)(wm * pinv)};
     }
@@ -38,10 +39,7 @@ struct TableBuilder {
 template <typename W>
 int build_tables(RingHost* rh, RingDev<W>* out) {
     const uint64_t p = rh->p;
-    // companion = wM * pinv, with pinv = -p^-1 for the F30 (REDC) field
-    W pinv = inv_word<W>((W)p);
-    if (rh->kind == 0) pinv = (W)(0u - pinv);
-    TableBuilder<W> tb{p, (int)(8 * sizeof(W)), pinv, 0};
+    TableBuilder<W> tb{p, (int)(8 * sizeof(W)), inv_word<W>((W)p), rh->kind == 0};
     // omega_[k] = top^(2^(K-k))
     std::vector<uint64_t> lvl(rh->K + 1), ilvl(rh->K + 1);
     uint64_t itop = powmod(rh->top, p - 2, p);
@@ -88,6 +86,12 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
         for (int i = 0; i < k; i++) { r = (r << 1) | (t & 1); t >>= 1; }
         return k <= rh->K ? powmod(lvl[k], r, p) : 0;
     };
+    // three variants: plain; every column scaled by 2^-CL (all
+    // rows come from unscaled chunk inverses); all but the last column scaled
+    // (the last row comes from the solved partial chunk, already exact)
+    const int CLs = sizeof(W) == 4 ? 14 : 13;
+    const uint64_t sc = powmod((p + 1) >> 1, CLs, p);
+    std::vector<Tw<W>> blocks[3];
     for (int m = 1; m <= 8; m++) {
         std::vector<uint64_t> A(m * 2 * m, 0);
         for (int r = 0; r < m; r++) {
@@ -110,23 +114,24 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
                     A[r * 2 * m + k] = (A[r * 2 * m + k] + p - mulmod(f, A[c * 2 * m + k], p)) % p;
             }
         }
-        for (int r = 0; r < 8; r++)
-            for (int c = 0; c < 8; c++)
-                host.push_back(tb.tw(ok && r < m && c < m ? A[r * 2 * m + m + c] : 0));
-        uint64_t wn = omega_s(m), pw = 1;
-        for (int c = 0; c < 8; c++) {
-            host.push_back(tb.tw(ok && c < m ? pw : 0));
-            pw = mulmod(pw, wn, p);
+        for (int var = 0; var < 3; var++) {
+            for (int r = 0; r < 8; r++)
+                for (int c = 0; c < 8; c++) {
+                    uint64_t e = ok && r < m && c < m ? A[r * 2 * m + m + c] : 0;
+                    if (var == 1 || (var == 2 && c < m - 1)) e = mulmod(e, sc, p);
+                    blocks[var].push_back(tb.tw(e));
+                }
+            uint64_t wn = omega_s(m), pw = 1;
+            for (int c = 0; c < 8; c++) {
+                blocks[var].push_back(tb.tw(ok && c < m ? pw : 0));
+                pw = mulmod(pw, wn, p);
+            }
         }
     }
+    for (int var = 0; var < 3; var++) host.insert(host.end(), blocks[var].begin(), blocks[var].end());
     size_t tw_bytes = host.size() * sizeof(Tw<W>);
-    const size_t nwords = 2 * nz + 2 * nh;
-    CK(cudaMalloc(&rh->dmem, tw_bytes + nwords * sizeof(W)));
+    CK(cudaMalloc(&rh->dmem, tw_bytes));
     CK(cudaMemcpy(rh->dmem, host.data(), tw_bytes, cudaMemcpyHostToDevice));
-    std::vector<W> words(nwords);
-    for (size_t j = 0; j < nwords; j++) words[j] = host[j].w;  // zf, zi, zfh, zih in order
-    W* dw = (W*)((char*)rh->dmem + tw_bytes);
-    CK(cudaMemcpy(dw, words.data(), nwords * sizeof(W), cudaMemcpyHostToDevice));
     Tw<W>* d = (Tw<W>*)rh->dmem;
     out->Zf = d;
     out->Zi = d + nz;
@@ -134,14 +139,12 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     out->Zih = d + 2 * nz + nh;
     out->ipow2 = d + 2 * nz + 2 * nh;
     out->vinv = d + 2 * nz + 2 * nh + 64;
-    out->Zwf = dw;
-    out->Zwi = dw + nz;
-    out->Zwfh = dw + 2 * nz;
-    out->Zwih = dw + 2 * nz + nh;
+    out->vinvS = out->vinv + 8 * 72;
+    out->vinvT = out->vinv + 16 * 72;
     uint64_t R1 = tb.to_m(1);
-    out->r2 = tb.tw(R1);  // Montgomery form of R is R^2 mod p
+    out->r2w = (W)tb.to_m(R1);  // R^2 mod p
     out->inv2 = tb.tw(inv2);
-    out->oneM = (W)R1;
+    out->oneW = tb.shoup ? (W)1 : (W)R1;
     out->zb = zb;
     out->zh = zh;
     return 0;
@@ -156,6 +159,17 @@ int get_ring(uint64_t p, uint64_t top, int K, RingHost** out) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_ring_mu);
+    static std::map<int, bool> pool_tuned;
+    if (!pool_tuned[dev]) {
+        // keep freed stream-ordered allocations cached: re-mapping GBs of
+        // scratch costs ~40 ms per call otherwise (measured)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_tuned[dev] = true;
+    }
     auto key = std::make_tuple(p, top, K, dev);
     auto it = g_rings.find(key);
     if (it != g_rings.end()) {
@@ -285,6 +299,82 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     return 0;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Host-batch pipeline: the batch is cut into sub-batches of consecutive
+// vectors; each sub-batch's H2D copy, word conversion, transform, conversion
+// back and D2H copy are issued on one of three streams, so PCIe traffic in
+// both directions overlaps the kernels of neighbouring sub-batches.
+constexpr int kPipeStreams = 3;
+
+cudaStream_t* pipe_streams() {
+    static std::mutex mu;
+    static std::map<int, std::vector<cudaStream_t>> per_dev;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto& v = per_dev[dev];
+    if (v.empty()) {
+        v.resize(kPipeStreams);
+        for (auto& st : v) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    }
+    return v.data();
+}
+
+template <class F>
+int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64_t>& o, const int64_t* len,
+                        int64_t count, int64_t lo, int64_t span, int inverse) {
+    using W = typename F::W;
+    const bool narrow = sizeof(W) == 4;
+    Scratch buf;
+    if (buf.get((size_t)span * 8 + (narrow ? (size_t)span * 4 : 0), nullptr)) return -1;
+    CK(cudaStreamSynchronize(nullptr));
+    uint64_t* d64 = (uint64_t*)buf.p;
+    W* dw = narrow ? (W*)(d64 + span) : (W*)d64;
+    // sub-batches of ~span/12 words (at least 2^22), consecutive vectors
+    const int64_t target = std::max<int64_t>(span / 12, 1 << 22);
+    std::vector<std::pair<int64_t, int64_t>> subs;
+    for (int64_t v0 = 0; v0 < count;) {
+        int64_t v1 = v0, words = 0;
+        while (v1 < count && (words < target || v1 == v0)) words += len[v1++];
+        subs.push_back({v0, v1});
+        v0 = v1;
+    }
+    std::vector<std::unique_ptr<PlanImpl>> plans;
+    for (auto& sb : subs) {
+        plans.emplace_back(new PlanImpl());
+        if (plan_create<F>(rh, sb.second - sb.first, 0, 0, o.data() + sb.first, len + sb.first, plans.back().get()))
+            return -1;
+    }
+    cudaStream_t* ss = pipe_streams();
+    for (size_t b = 0; b < subs.size(); b++) {
+        cudaStream_t st = ss[b % kPipeStreams];
+        const int64_t a0 = o[subs[b].first];
+        const int64_t a1 = o[subs[b].second - 1] + len[subs[b].second - 1];
+        const int64_t nw = a1 - a0;
+        CK(cudaMemcpyAsync(d64 + a0, x + lo + a0, (size_t)nw * 8, cudaMemcpyHostToDevice, st));
+        const int nb = (int)std::min<int64_t>((nw + 255) / 256, 148 * 8);
+        if (narrow) {
+            k_u64_to_w<W><<<nb, 256, 0, st>>>(d64 + a0, dw + a0, nw);
+            g_launches++;
+        }
+        if (plan_exec<F>(plans[b].get(), dw, inverse, nullptr, st)) return -1;
+        if (narrow) {
+            k_w_to_u64<W><<<nb, 256, 0, st>>>(dw + a0, d64 + a0, nw);
+            g_launches++;
+        }
+        CK(cudaMemcpyAsync(x + lo + a0, d64 + a0, (size_t)nw * 8, cudaMemcpyDeviceToHost, st));
+    }
+    for (int i = 0; i < kPipeStreams; i++) CK(cudaStreamSynchronize(ss[i]));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int64_t count, uint64_t p,
                        uint64_t top, int K, int inverse) {
     if (count <= 0) return 0;
@@ -293,15 +383,25 @@ int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int6
     if (get_ring(p, top, K, &rh)) return -1;
     std::vector<int64_t> o(count);
     int64_t lo = INT64_MAX, hi = 0, acc = 0;
+    bool sorted = true;
     for (int64_t v = 0; v < count; v++) {
         if (len[v] <= 0 || (K < 62 && len[v] > (1ll << K))) return fail("vector length outside [1, 2^K]");
         o[v] = off ? off[v] : acc;
+        if (v && o[v] < o[v - 1] + len[v - 1]) sorted = false;
         acc += len[v];
         lo = std::min(lo, o[v]);
         hi = std::max(hi, o[v] + len[v]);
     }
     const int64_t span = hi - lo;
     for (auto& e : o) e -= lo;
+    if (sorted) {
+        switch (rh->kind) {
+            case 0: return host_batch_pipeline<F30>(rh, x, o, len, count, lo, span, inverse);
+            case 1: return host_batch_pipeline<F32>(rh, x, o, len, count, lo, span, inverse);
+            default: return host_batch_pipeline<F62>(rh, x, o, len, count, lo, span, inverse);
+        }
+    }
+    // overlapping / unsorted layouts: one stream, whole span
     cudaStream_t st = nullptr;
     const size_t wb = rh->wbytes;
     Scratch buf;

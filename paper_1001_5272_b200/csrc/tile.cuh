@@ -39,42 +39,41 @@ struct RingDev {
     const Tw<W>* Zfh;   // Zfh[i] = omega_{2 i 2^zb}, i < 2^zh
     const Tw<W>* Zih;
     const Tw<W>* ipow2; // ipow2[k] = 2^-k, k < 64
-    const W* Zwf;       // Montgomery words of Zf / Zi alone (companion recomputed
-    const W* Zwi;       //   with one multiply: halves twiddle traffic)
-    const W* Zwfh;      // Montgomery words of Zfh / Zih
-    const W* Zwih;
     const Tw<W>* vinv;  // 8 blocks of 72: V_m^-1 (m x m, V_m[s][i] = omega_s^i), then omega_m^i
-
-    Tw<W> r2;           // R^2 mod p (Montgomery form of R): mont(x, r2.w) = x R
+    const Tw<W>* vinvS; // same with every column times 2^-CL
+    const Tw<W>* vinvT; // same with all but the last column times 2^-CL
     Tw<W> inv2;         // 1/2
-    W oneM;             // R mod p (Montgomery form of 1)
+    W r2w;              // R^2 mod p as a raw word: mont(mont(a, b), r2w) = a b
+    W oneW;             // 1 as a field word (1, or R mod p for Montgomery fields)
     int zb, zh;
 };
 
-// omega_{2J} for an arbitrary J < 2^(zb+zh), Montgomery form, canonical.
+// omega_{2J} for an arbitrary J < 2^(zb+zh), as a canonical field word.
 template <class F>
 TFT_DEV typename F::W zbig(const F& f, const RingDev<typename F::W>& R, uint64_t J, bool inverse) {
     const Tw<typename F::W>* lo = inverse ? R.Zi : R.Zf;
     const Tw<typename F::W>* hi = inverse ? R.Zih : R.Zfh;
     uint64_t m = (1ull << R.zb) - 1;
     if (J <= m) return lo[J].w;
-    return f.red1(f.mont(hi[J >> R.zb].w, lo[J & m].w));
+    return f.twmul(hi[J >> R.zb], lo[J & m]);
 }
 
-// omega_s (modring.py:223-234) in Montgomery form: omega_{2j+1} = -omega_{2j}.
+// omega_s (modring.py:223-234) as a field word: omega_{2j+1} = -omega_{2j}.
 template <class F>
-TFT_DEV typename F::W omega_m(const F& f, const RingDev<typename F::W>& R, uint64_t s) {
+TFT_DEV typename F::W omega_w(const F& f, const RingDev<typename F::W>& R, uint64_t s) {
     typename F::W w = zbig(f, R, s >> 1, false);
     return (s & 1) ? f.p - w : w;
 }
 
+// base^e for a field word base (square and multiply on twiddles)
 template <class F>
-TFT_DEV typename F::W pow_m(const F& f, typename F::W baseM, typename F::W oneM, uint64_t e) {
-    typename F::W r = oneM;
+TFT_DEV typename F::W pow_w(const F& f, typename F::W base, typename F::W one, uint64_t e) {
+    typename F::W r = one;
+    Tw<typename F::W> b = f.tw(base);
     while (e) {
-        if (e & 1) r = f.red1(f.mont(r, baseM));
-        baseM = f.red1(f.mont(baseM, baseM));
+        if (e & 1) r = f.twmul(f.tw(r), b);
         e >>= 1;
+        if (e) b = f.tw(f.twmul(b, b));
     }
     return r;
 }
@@ -88,21 +87,6 @@ struct TwPrefix {  // untwisted tile: theta(s, J) = Z[J]
     TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
 #pragma unroll
         for (int q = 0; q < N; ++q) out[q] = Z[J0 + q];
-    }
-};
-
-template <class F>
-struct TwHeap {  // twisted tile: stage s table at [2^(t-s-1), 2^(t-s)) of T
-    const typename F::W* T;
-    int t;
-    F f;
-    TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
-        return f.mk(T[(1u << (t - s - 1)) + J]);
-    }
-    template <int N>
-    TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
-#pragma unroll
-        for (int q = 0; q < N; ++q) out[q] = get(s, J0 + q);
     }
 };
 
@@ -120,10 +104,11 @@ TFT_DEV void reg_fwd(const F& f, typename F::W* v, uint32_t base, int slo, const
     tp.template get_many<NQ>(s, base >> (s + 1), w);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
+        const Tw<W> t = w[q];
 #pragma unroll
         for (int r = 0; r < (1 << ST); ++r) {
             const int i = (q << (ST + 1)) | r;
-            f.fwd(v[i], v[i | (1 << ST)], w[q]);
+            f.fwd(v[i], v[i | (1 << ST)], t);
         }
     }
     if constexpr (ST > 0) reg_fwd<F, KK, ST - 1>(f, v, base, slo, tp);
@@ -145,12 +130,13 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
     const Tw<W> sc = ipow2[s + 1];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
+        const Tw<W> t = w[q];
 #pragma unroll
         for (int r = 0; r < (1 << ST); ++r) {
             const int i = (q << (ST + 1)) | r;
             const uint32_t pos = base + ((uint32_t)i << slo);
             if (MASK && pos >= hs) continue;
-            f.inv(v[i], v[i | (1 << ST)], w[q]);
+            f.inv(v[i], v[i | (1 << ST)], t);
             if (MASK ? pos >= hs1 : scale_all) {
                 v[i] = f.mulw(v[i], sc);
                 v[i | (1 << ST)] = f.mulw(v[i | (1 << ST)], sc);
@@ -158,25 +144,6 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
         }
     }
     if constexpr (ST + 1 < KK) reg_inv<F, KK, ST + 1, MASK>(f, v, base, slo, tp, h, last, ipow2);
-}
-
-// Fill the heap table of block B (level t): T[2^(t-s-1) + J] = omega_{2(B 2^(t-s-1) + J)}
-// = omega_{2 B 2^(t-s-1)} * omega_{2J} (product rule).
-// `zeta` is scratch for t words.  Ends with __syncthreads().
-template <class F>
-TFT_DEV void build_heap(const F& f, const RingDev<typename F::W>& R, typename F::W* T,
-                        typename F::W* zeta, int t, uint64_t B, bool inverse) {
-    using W = typename F::W;
-    for (int s = threadIdx.x; s < t; s += blockDim.x) zeta[s] = zbig(f, R, B << (t - s - 1), inverse);
-    __syncthreads();
-    const Tw<W>* Z = inverse ? R.Zi : R.Zf;
-    for (uint32_t idx = threadIdx.x + 1; idx < (1u << t); idx += blockDim.x) {
-        int lev = 31 - __clz(idx);
-        int s = t - 1 - lev;
-        uint32_t J = idx - (1u << lev);
-        T[idx] = f.red1(f.mont(zeta[s], Z[J].w));
-    }
-    __syncthreads();
 }
 
 // ---------------------------------------------------------------- rounds
@@ -369,23 +336,23 @@ TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h,
 }
 
 // Per-column evaluation sum_{i<K} S[i] w^i (the first virtual output of a
-// column whose K coefficients are now known).  Result per column into out[col]
-// (canonical).  `red` is scratch of blockDim.x words.  Ends synced.
+// column whose K coefficients are now known); w a canonical field word.
+// Result per column into out[col] (canonical).  `red` is scratch of
+// blockDim.x words.  Ends synced.
 template <class F>
-TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t K,
-                        typename F::W wM, typename F::W oneM, typename F::W* red,
-                        typename F::W* out) {
+TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t K, typename F::W wword,
+                        typename F::W one, typename F::W* red, typename F::W* out) {
     using W = typename F::W;
     const uint32_t ncols = 1u << tl.wlog;
     const uint32_t nparts = blockDim.x >> tl.wlog;
     const uint32_t col = threadIdx.x & (ncols - 1), part = threadIdx.x >> tl.wlog;
     const uint32_t e = (K + nparts - 1) / nparts;
     const uint32_t r0 = part * e, r1 = min(K, r0 + e);
-    const Tw<W> w = f.mk(wM);
+    const Tw<W> w = f.tw(wword);
     W acc = 0;
     if (r0 < r1) {
         for (uint32_t i = r1; i-- > r0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(i, col))));
-        acc = f.cmulw(acc, f.mk(pow_m(f, wM, oneM, r0)));
+        acc = f.cmulw(acc, f.tw(pow_w(f, wword, one, r0)));
     }
     red[threadIdx.x] = acc;
     __syncthreads();

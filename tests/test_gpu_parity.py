@@ -214,3 +214,19 @@ def test_tile_plain_inverse_every_size():
         d = device.to_words(y, cfg)
         backend.check(f(cfg.p, cfg.omegaK, cfg.K, d.data_ptr(), t))
         assert np.array_equal(device.from_words(d, cfg), O.itft(y, cfg.p, cfg.omegaK, cfg.K)), t
+
+
+def test_host_batch_pipeline_against_oracle():
+    """tftb_tft_batch_u64 (pipelined host batch) on a ragged batch, both directions."""
+    import ctypes
+    cfg = T.default_config()
+    rng = np.random.default_rng(21)
+    lens = rng.integers(1, 90000, 300).astype(np.int64)
+    flat = rng.integers(0, cfg.p, int(lens.sum()), dtype=np.uint64)
+    x = flat.copy()
+    lib = backend.load()
+    lp = lens.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    backend.check(lib.tftb_tft_batch_u64(x.ctypes.data, None, lp, lens.size, cfg.p, cfg.omegaK, cfg.K, 0))
+    assert np.array_equal(x, O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K))
+    backend.check(lib.tftb_tft_batch_u64(x.ctypes.data, None, lp, lens.size, cfg.p, cfg.omegaK, cfg.K, 1))
+    assert np.array_equal(x, flat)
