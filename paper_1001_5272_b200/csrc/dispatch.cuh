@@ -78,7 +78,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
     a.stash = stash_buf ? stash_buf : (W*)stash.p;
     constexpr int CL = Limits<F>::CL;
-    const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 64) * sizeof(W);
+    const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
     if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F, CL>, sm_chunk) ||
         set_smem(k_chunk_inv<F, CL>, sm_chunk) || set_smem(k_last_inv<F, CL>, sm_chunk))

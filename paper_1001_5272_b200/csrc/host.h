@@ -137,7 +137,8 @@ int make_plan(int64_t n, Plan* pl) {
     // rest, as many adjacent columns per CTA as fit a 2^col_t-word tile
     int l1 = CL;
     int l0 = l - l1;
-    int wlog = std::max(0, std::min(4, Limits<F>::col_t - l0));
+    // up to 256 adjacent columns (colsum_pow needs blockDim >= columns)
+    int wlog = std::max(0, std::min(8, Limits<F>::col_t - l0));
     if (l0 + wlog > Limits<F>::col_t) return fail("transform length too large for the two-pass plan");
     pl->l0 = l0;
     pl->l1 = l1;
