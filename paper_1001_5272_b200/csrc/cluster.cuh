@@ -105,74 +105,92 @@ struct TwBig {
 };
 
 // ------------------------------------------------------ compile-time rounds
-template <int SLO>
-struct PhysStep {
-    static constexpr uint32_t v = SLO >= 5 ? (1u << SLO) + (1u << (SLO - 5)) : (1u << SLO);
-};
+// A tile of 2^TL rows x 2^WLOG interleaved columns, element (pos, col) at
+// index (pos << WLOG) | col, physical slot idx + idx/32.  A unit is 2^KK
+// words of one column at rows base + i 2^SLO.  Its physical offsets are
+// compile-time constants in every case the round schedule produces (SLO = 0
+// or SLO >= 5):
+//   SLO+WLOG >= 5          : i (2^(SLO+WLOG) + 2^(SLO+WLOG-5))
+//   SLO = 0, KK+WLOG <= 5  : i 2^WLOG         (unit inside one 32-word row)
+//   SLO = 0, KK+WLOG > 5   : i 2^WLOG + (i >> (5-WLOG))
+template <int SLO, int WLOG, int KK>
+TFT_DEV constexpr uint32_t unit_off(int i) {
+    return (SLO + WLOG >= 5) ? (uint32_t)i * ((1u << (SLO + WLOG)) + (1u << (SLO + WLOG - 5)))
+           : (KK + WLOG <= 5) ? ((uint32_t)i << WLOG)
+                              : (((uint32_t)i << WLOG) + ((uint32_t)i >> (5 - WLOG)));
+}
 
-template <class F, int TL, int KK, int SLO, class TP>
-TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp) {
+// Forward round.  With PRUNE, units whose every output row is >= lim are
+// skipped (only rows < lim are needed after the remaining stages).
+template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
+TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need) {
     using W = typename F::W;
-    constexpr uint32_t NU = 1u << (TL - KK);
-    constexpr uint32_t STEP = PhysStep<SLO>::v;
-    for (uint32_t u = threadIdx.x; u < NU; u += blockDim.x) {
+    constexpr uint32_t NU = 1u << (TL - KK + WLOG);
+    const uint32_t lim = PRUNE ? ((need + (1u << SLO) - 1) >> SLO) << SLO : 0;
+    for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
+        const uint32_t col = g & ((1u << WLOG) - 1), u = g >> WLOG;
         const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
-        W* pb = S + base + (base >> 5);
+        if (PRUNE && base >= lim) continue;
+        const uint32_t idx0 = (base << WLOG) | col;
+        W* pb = S + idx0 + (idx0 >> 5);
         W v[1 << KK];
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
+        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];
         reg_fwd<F, KK, KK - 1>(f, v, base, SLO, tp);
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
+        for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
     }
 }
 
-// unmasked inverse round; the tile's last stage (s = TL-1) also scales by 2^-TL
-template <class F, int TL, int KK, int SLO, bool MASK, class TP, bool SCALE = true>
+// Inverse round (stages ascending).  MASK: only pairs inside complete binary
+// blocks of [0, h) run, each block scaled at its last stage (tile.cuh
+// reg_inv); SCALE=false leaves an unmasked tile scaled by 2^TL.
+template <class F, int TL, int KK, int SLO, int WLOG, bool MASK, bool SCALE, class TP>
 TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
                           uint32_t h) {
     using W = typename F::W;
-    constexpr uint32_t NU = 1u << (TL - KK);
-    constexpr uint32_t STEP = PhysStep<SLO>::v;
+    constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t h_lo = MASK ? (uint32_t)(((uint64_t)h >> (SLO + 1)) << (SLO + 1)) : 0;
-    for (uint32_t u = threadIdx.x; u < NU; u += blockDim.x) {
+    for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
+        const uint32_t col = g & ((1u << WLOG) - 1), u = g >> WLOG;
         const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
         if (MASK && base >= h_lo) continue;
-        W* pb = S + base + (base >> 5);
+        const uint32_t idx0 = (base << WLOG) | col;
+        W* pb = S + idx0 + (idx0 >> 5);
         W v[1 << KK];
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
+        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];
         reg_inv<F, KK, 0, MASK>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
+        for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
     }
 }
 
 // stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),
 // recursing down to a final 5-or-fewer-stage round at s_lo = 0.
-template <class F, int TL, int SHI, class TP>
-TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp) {
+template <class F, int TL, int SHI, int WLOG = 0, bool PRUNE = false, class TP>
+TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need = 0) {
     if constexpr (SHI <= 5) {
-        fwd_round_ct<F, TL, SHI, 0>(f, S, tp);
+        fwd_round_ct<F, TL, SHI, 0, WLOG, PRUNE>(f, S, tp, need);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        fwd_round_ct<F, TL, KK, SHI - KK>(f, S, tp);
+        fwd_round_ct<F, TL, KK, SHI - KK, WLOG, PRUNE>(f, S, tp, need);
         __syncthreads();
-        fwd_rounds_ct<F, TL, SHI - KK>(f, S, tp);
+        fwd_rounds_ct<F, TL, SHI - KK, WLOG, PRUNE>(f, S, tp, need);
     }
 }
 
-template <class F, int TL, int SHI, bool MASK, class TP, bool SCALE = true>
+template <class F, int TL, int SHI, bool MASK, class TP, bool SCALE = true, int WLOG = 0>
 TFT_DEV void inv_rounds_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
                            uint32_t h = 0) {
     if constexpr (SHI <= 5) {
-        inv_round_ct<F, TL, SHI, 0, MASK, TP, SCALE>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, SHI, 0, WLOG, MASK, SCALE>(f, S, tp, ipow2, h);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        inv_rounds_ct<F, TL, SHI - KK, MASK, TP, SCALE>(f, S, tp, ipow2, h);
-        inv_round_ct<F, TL, KK, SHI - KK, MASK, TP, SCALE>(f, S, tp, ipow2, h);
+        inv_rounds_ct<F, TL, SHI - KK, MASK, TP, SCALE, WLOG>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, KK, SHI - KK, WLOG, MASK, SCALE>(f, S, tp, ipow2, h);
         __syncthreads();
     }
 }
@@ -263,7 +281,8 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     }
     cl.sync();
 
-    fwd_rounds_ct<F, CL, CL>(f, S, TwDirect<F>{a.R.Zf, g, CL, f});
+    // only this chunk's rows below n are outputs: prune the rest
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f}, (uint32_t)min((int64_t)C, n - cbase));
 
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
@@ -401,7 +420,8 @@ __global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
     const int64_t avail = n - cbase;
     tile_load<W>(S, x, avail, C, [&](uint32_t i, W w) { return (int64_t)i < avail ? w : st[i]; });
     __syncthreads();
-    fwd_rounds_ct<F, CL, CL>(f, S, TwBig<F>{a.R.Zf, a.R.Zfh, k, CL, a.R.zb, f});
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwBig<F>{a.R.Zf, a.R.Zfh, k, CL, a.R.zb, f},
+                                      (uint32_t)min((int64_t)C, avail));
     tile_store<W>(x, S, (uint32_t)min((int64_t)C, avail), [&](W w) { return f.canon(w); });
 }
 
@@ -457,4 +477,131 @@ __global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
     SmemTile<W> tl{S, CL, 0};
     itft_phases23(f, tl, h, tpf, tpi, a.R);
     tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });
+}
+
+// ================================================ two-pass plan, column pass
+// Columns are nodes (c, l1) of the reference tree: rows r at positions
+// r 2^l1 + c.  One CTA owns 2^WLOG adjacent columns of 2^L0 rows.
+template <class F>
+__host__ __device__ constexpr int col_tile_log() { return sizeof(typename F::W) == 4 ? 14 : 13; }
+template <class F, int L0>
+__host__ __device__ constexpr int col_wlog() {
+    return (col_tile_log<F>() - L0) < 0 ? 0 : ((col_tile_log<F>() - L0) > 8 ? 8 : (col_tile_log<F>() - L0));
+}
+
+// S[(r << WLOG) | col] = xf(r, col, valid ? src[r*C + col] : 0), valid = r*C + col < avail;
+// 16-byte loads along rows when the rows are 16-byte aligned, UNR in flight.
+template <typename W, int L0, int WLOG, int UNR = 8, class XF>
+TFT_DEV void col_load(W* S, const W* src, uint32_t C, int64_t avail, const XF& xf) {
+    constexpr int NV = 16 / sizeof(W);
+    constexpr uint32_t R = 1u << L0, NC = 1u << WLOG;
+    const bool vec = (NC % NV == 0) && (((uintptr_t)src & 15) == 0) && (C % NV == 0);
+    if (vec) {
+        constexpr uint32_t QPR = NC / NV;  // quads per row
+        const uint32_t nq = R * QPR;
+        for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
+            typename Vec16<W>::T buf[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t q = q0 + u * blockDim.x;
+                const uint32_t r = q / QPR, c = (q % QPR) * NV;
+                const int64_t pos = (int64_t)r * C + c;
+                if (q < nq && pos + NV <= avail) {
+                    buf[u] = ld_stream(reinterpret_cast<const typename Vec16<W>::T*>(src + pos));
+                } else {
+                    W e[NV];
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) e[k] = (q < nq && pos + k < avail) ? src[pos + k] : W(0);
+                    buf[u] = Vec16<W>::make(e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t q = q0 + u * blockDim.x;
+                if (q >= nq) break;
+                const uint32_t r = q / QPR, c = (q % QPR) * NV;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const uint32_t idx = (r << WLOG) | (c + k);
+                    S[idx + (idx >> 5)] = xf(r, c + k, Vec16<W>::get(buf[u], k));
+                }
+            }
+        }
+    } else {
+        for (uint32_t g = threadIdx.x; g < (R << WLOG); g += blockDim.x) {
+            const uint32_t r = g >> WLOG, c = g & (NC - 1);
+            const int64_t pos = (int64_t)r * C + c;
+            S[g + (g >> 5)] = xf(r, c, pos < avail ? src[pos] : W(0));
+        }
+    }
+}
+
+template <class F, int L0>
+__global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    constexpr int WLOG = col_wlog<F, L0>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const int l1 = a.l1;
+    if (ceil_lg_dev(n) - l1 != L0) return;
+    const uint32_t C = 1u << l1, c0 = blockIdx.x << WLOG;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    col_load<W, L0, WLOG>(S, in + c0, C, nin - c0, [](uint32_t, uint32_t, W w) { return w; });
+    __syncthreads();
+    // rows <= K are the only outputs (row K: real for c < h, the stash for c >= h)
+    fwd_rounds_ct<F, L0, L0, WLOG, true>(f, S, TwPrefix<F>{a.R.Zf}, K + (h ? 1u : 0u));
+    const uint32_t NC = 1u << WLOG;
+    W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    for (uint32_t g = threadIdx.x; g < ((K + 1) << WLOG) && g < (1u << (L0 + WLOG)); g += blockDim.x) {
+        const uint32_t r = g >> WLOG, c = c0 + (g & (NC - 1));
+        const int64_t pos = (int64_t)r * C + c;
+        if (pos < n) x[pos] = f.canon(S[g + (g >> 5)]);
+        else if (h && r == K) st[c] = f.canon(S[g + (g >> 5)]);
+    }
+}
+
+// inverse steps 2 (which = 0: columns c >= h, K rows, stash their row K) and
+// 4 (which = 1: columns c < h, K+1 rows).  grid: (C >> WLOG, vectors)
+template <class F, int L0>
+__global__ void __launch_bounds__(256) k_colc_inv(LaunchArgs<F> a, int which) {
+    using W = typename F::W;
+    constexpr int WLOG = col_wlog<F, L0>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1;
+    if (ceil_lg_dev(n) - l1 != L0) return;
+    const uint32_t C = 1u << l1, c0 = blockIdx.x << WLOG, NC = 1u << WLOG;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    const uint32_t lo = which == 0 ? h : 0, hi = which == 0 ? C : h;
+    if (c0 + NC <= lo || c0 >= hi) return;
+    const uint32_t rows = which == 0 ? K : K + 1;
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v);
+    col_load<W, L0, WLOG>(S, x + c0, C, n - c0, [&](uint32_t r, uint32_t, W w) { return r < rows ? w : W(0); });
+    __syncthreads();
+    const TwPrefix<F> tpf{a.R.Zf}, tpi{a.R.Zi};
+    inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, WLOG>(f, S, tpi, a.R.ipow2, rows);
+    SmemTile<W> tl{S, L0, WLOG};
+    itft_phases23(f, tl, rows, tpf, tpi, a.R);
+    for (uint32_t g = threadIdx.x; g < (rows << WLOG); g += blockDim.x) {
+        const uint32_t r = g >> WLOG, c = c0 + (g & (NC - 1));
+        const int64_t pos = (int64_t)r * C + c;
+        if (c >= lo && c < hi && pos < n) x[pos] = f.canon(S[g + (g >> 5)]);
+    }
+    if (which == 0 && h) {
+        W* red = S + padded_words(1u << (L0 + WLOG));
+        W* nv = red + blockDim.x;
+        colsum_pow(f, tl, K, omega_w(f, a.R, K), a.R.oneW, red, nv);
+        for (uint32_t col = threadIdx.x; col < NC; col += blockDim.x) {
+            const uint32_t c = c0 + col;
+            if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
+        }
+    }
 }

@@ -80,23 +80,40 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     constexpr int CL = Limits<F>::CL;
     const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
-    if (set_smem(k_col_fwd<F>, sm_col) || set_smem(k_col_inv<F>, sm_col) || set_smem(k_chunk_fwd<F, CL>, sm_chunk) ||
-        set_smem(k_chunk_inv<F, CL>, sm_chunk) || set_smem(k_last_inv<F, CL>, sm_chunk))
+    if (set_smem(k_chunk_fwd<F, CL>, sm_chunk) || set_smem(k_chunk_inv<F, CL>, sm_chunk) ||
+        set_smem(k_last_inv<F, CL>, sm_chunk))
         return -1;
+    // compile-time column kernels, one instantiation per l0
+    void (*colf)(LaunchArgs<F>) = nullptr;
+    void (*coli)(LaunchArgs<F>, int) = nullptr;
+    switch (pl.l0) {
+#define TFTB_COL(L)                     \
+    case L:                             \
+        colf = k_colc_fwd<F, L>;        \
+        coli = k_colc_inv<F, L>;        \
+        break;
+        TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
+        TFTB_COL(10) TFTB_COL(11) TFTB_COL(12) TFTB_COL(13) TFTB_COL(14)
+#undef TFTB_COL
+        default: return fail("no column kernel for this plan");
+    }
+    if (col_wlog<F, 4>() >= 0 && pl.wlog != std::max(0, std::min(8, Limits<F>::col_t - pl.l0)))
+        return fail("column plan mismatch");
+    if (set_smem(colf, sm_col) || set_smem(coli, sm_col)) return -1;
     for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
         a.vbase = v0;
         unsigned nv = (unsigned)std::min(count - v0, vchunk);
         dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
         if (!inverse) {
-            k_col_fwd<F><<<gcol, kNT, sm_col, st>>>(a);
+            colf<<<gcol, kNT, sm_col, st>>>(a);
             k_chunk_fwd<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
             g_launches += 2;
         } else {
             static const int stop = getenv("TFTB_DEBUG_STOP") ? atoi(getenv("TFTB_DEBUG_STOP")) : 9;  // debug knob
             if (stop >= 1) k_chunk_inv<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
-            if (stop >= 2) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 0);
+            if (stop >= 2) coli<<<gcol, kNT, sm_col, st>>>(a, 0);
             if (stop >= 3) k_last_inv<F, CL><<<glast, kNT, sm_chunk, st>>>(a);
-            if (stop >= 4) k_col_inv<F><<<gcol, kNT, sm_col, st>>>(a, 1);
+            if (stop >= 4) coli<<<gcol, kNT, sm_col, st>>>(a, 1);
             g_launches += 4;
         }
         CK(cudaGetLastError());
