@@ -437,8 +437,10 @@ __global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
     constexpr uint32_t C = 1u << CL;
     const int64_t v = a.vbase + blockIdx.y;
     const int64_t n = a.xd.n(v);
-    const uint32_t k = blockIdx.x;
     const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    // the partial chunk (longest CTA: masked rounds) takes block 0 so it does
+    // not become the grid's tail
+    const uint32_t k = !h ? blockIdx.x : (blockIdx.x == 0 ? K : blockIdx.x - 1);
     if (k > K || (k == K && !h)) return;
     const uint32_t len = k < K ? C : h;
     const F f = a.f;
