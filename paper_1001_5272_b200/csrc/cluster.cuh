@@ -270,8 +270,11 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     const F f = a.f;
 
     const int64_t cbase = (int64_t)g * C;
+    TFTB_STAMP(a, 0);
     tile_load<W>(S, in + cbase, nin - cbase, C, [](uint32_t, W w) { return w; });
+    TFTB_STAMP(a, 1);
     cl.sync();
+    TFTB_STAMP(a, 2);
 
     // cross stages: 2^gam-point untwisted column transforms over DSMEM
     switch (gam) {
@@ -279,13 +282,17 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
         case 2: cross_fwd<F, 2>(f, cl, S, g, G, C, a.R.Zf); break;
         default: cross_fwd<F, 3>(f, cl, S, g, G, C, a.R.Zf); break;
     }
+    TFTB_STAMP(a, 3);
     cl.sync();
+    TFTB_STAMP(a, 4);
 
     // only this chunk's rows below n are outputs: prune the rest
     fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f}, (uint32_t)min((int64_t)C, n - cbase));
+    TFTB_STAMP(a, 5);
 
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
+    TFTB_STAMP(a, 6);
 }
 
 // column solve: rows j < M of column `ph` (physical index) hold the column's
@@ -606,4 +613,115 @@ __global__ void __launch_bounds__(256) k_colc_inv(LaunchArgs<F> a, int which) {
             if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
         }
     }
+}
+
+// ===================================== forward for 2^CL < n <= 8 2^CL, no cluster
+// CTA g of vector v needs row g of every column's 2^GAM-point network.  It
+// reads the column's rows straight from global memory (the first CTA of a
+// vector brings them from HBM, its siblings hit L2) and evaluates only the
+// cone of row g: the top stage has theta = 1 (adds only), stage sp keeps the
+// half selected by bit sp of g with one twiddle omega_{2 (g >> (sp+1))}, so a
+// word costs at most GAM-1 products (<= 1 for config 2).  No DSMEM, no
+// cluster barrier; grid (G, vectors).
+template <class F, int GAM>
+TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, const Tw<typename F::W>* tw) {
+    using W = typename F::W;
+    constexpr int GP = 1 << GAM;
+    // top stage: theta = 1
+    {
+        constexpr int H = GP / 2;
+        const bool sel = (g >> (GAM - 1)) & 1;
+#pragma unroll
+        for (int i = 0; i < H; ++i) vals[i] = f.half1(vals[i], vals[i + H], sel);
+    }
+#pragma unroll
+    for (int sp = GAM - 2; sp >= 0; --sp) {
+        const int H = 1 << sp;
+        const bool sel = (g >> sp) & 1;
+        const Tw<W> t = tw[sp];
+#pragma unroll
+        for (int i = 0; i < H; ++i) vals[i] = f.half(vals[i], vals[i + H], t, sel);
+    }
+    return vals[0];
+}
+
+template <class F, int CL, int GAM>
+__global__ void __launch_bounds__(256, 3) k_clg_fwd(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    constexpr int GP = 1 << GAM;
+    constexpr int NV = 16 / sizeof(W);
+    const uint32_t g = blockIdx.x;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const int64_t cbase = (int64_t)g * C;
+    if (cbase >= n) return;
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    TFTB_STAMP(a, 0);
+    Tw<W> tw[GAM > 1 ? GAM - 1 : 1];
+#pragma unroll
+    for (int sp = 0; sp < GAM - 1; ++sp) tw[sp] = a.R.Zf[g >> (sp + 1)];
+    // rows j*C + i share their alignment (C is a multiple of the vector):
+    // scalar head up to 16-byte alignment, quads, scalar tail
+    const uint32_t mis = (uint32_t)(((uintptr_t)in & 15) / sizeof(W));
+    const uint32_t head = (NV - mis) % NV;
+    auto one = [&](uint32_t i) {
+        W vals[GP];
+#pragma unroll
+        for (int j = 0; j < GP; ++j) {
+            const int64_t pos = (int64_t)j * C + i;
+            vals[j] = pos < nin ? in[pos] : W(0);
+        }
+        S[i + (i >> 5)] = cone_row<F, GAM>(f, vals, g, tw);
+    };
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
+    {
+        constexpr int UNR = GP <= 4 ? 2 : 1;
+        const uint32_t nq = (C - head) / NV;
+        for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
+            typename Vec16<W>::T buf[UNR][GP];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t q = q0 + u * blockDim.x;
+#pragma unroll
+                for (int j = 0; j < GP; ++j) {
+                    const int64_t pos = (int64_t)j * C + head + (int64_t)q * NV;
+                    if (q < nq && pos + NV <= nin) {
+                        buf[u][j] = ld_stream(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
+                    } else {
+                        W e[NV];
+#pragma unroll
+                        for (int k = 0; k < NV; ++k) e[k] = (q < nq && pos + k < nin) ? in[pos + k] : W(0);
+                        buf[u][j] = Vec16<W>::make(e);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint32_t q = q0 + u * blockDim.x;
+                if (q >= nq) break;
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    W vals[GP];
+#pragma unroll
+                    for (int j = 0; j < GP; ++j) vals[j] = Vec16<W>::get(buf[u][j], k);
+                    const uint32_t i = head + q * NV + k;
+                    S[i + (i >> 5)] = cone_row<F, GAM>(f, vals, g, tw);
+                }
+            }
+        }
+        for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
+    }
+    TFTB_STAMP(a, 1);
+    __syncthreads();
+    TFTB_STAMP(a, 2);
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f}, (uint32_t)min((int64_t)C, n - cbase));
+    TFTB_STAMP(a, 5);
+    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
+    tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
+    TFTB_STAMP(a, 6);
 }

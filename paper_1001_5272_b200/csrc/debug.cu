@@ -54,3 +54,41 @@ extern "C" int tftb_debug_itft_tile(uint64_t p, uint64_t top, int K, void* data,
     CK(cudaDeviceSynchronize());
     return 0;
 }
+
+// Phase timestamps of the cluster forward on a uniform batch (count vectors of
+// length n): out[cta*8 + k], k = 0 start, 1 loaded, 2 synced, 3 cross done,
+// 4 synced, 5 rounds done, 6 stored.
+extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* data, int64_t n, int64_t count,
+                                         unsigned long long* out) {
+    using namespace tftb;
+    RingHost* rh;
+    if (get_ring(p, top, K, &rh)) return -1;
+    if (rh->kind != 0) return fail("debug: F30 only");
+    Plan pl;
+    if (make_plan<F30>(n, &pl) || pl.kind != kCluster) return fail("debug: n must use the cluster plan");
+    LaunchArgs<F30> a{};
+    a.f = make_field<F30>(p);
+    a.R = rh->r32;
+    a.x = (uint32_t*)data;
+    a.in = a.x;
+    a.xd = VecDesc<uint32_t>{nullptr, nullptr, n, n};
+    a.ind = a.xd;
+    a.timing = out;
+    constexpr int CL = Limits<F30>::CL;
+    const size_t smem = padded_words(1u << CL) * 4;
+    if (set_smem(k_cl_fwd<F30, CL>, smem)) return -1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(pl.G, (unsigned)count, 1);
+    lc.blockDim = dim3(256, 1, 1);
+    lc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pl.G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F30, CL>, a));
+    CK(cudaDeviceSynchronize());
+    return 0;
+}

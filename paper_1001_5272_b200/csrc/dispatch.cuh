@@ -47,8 +47,20 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (inverse) CK(cudaLaunchKernelEx(&lc, ki, a));
-            else CK(cudaLaunchKernelEx(&lc, kf, a));
+            static const bool dsmem_fwd = getenv("TFTB_FWD_DSMEM") != nullptr;  // A/B knob
+            if (inverse) {
+                CK(cudaLaunchKernelEx(&lc, ki, a));
+            } else if (dsmem_fwd) {
+                CK(cudaLaunchKernelEx(&lc, kf, a));
+            } else {
+                // no-cluster forward: rows re-read through L2 instead of DSMEM
+                const int gam = pl.l - CL;
+                void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
+                                           : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
+                if (set_smem(kg, smem)) return -1;
+                kg<<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+            }
             g_launches++;
         }
         return 0;

@@ -72,6 +72,15 @@ struct F30 {
         x = s;
         y = mulw(d, t);
     }
+    // one output of the butterfly: sel ? a - w b : a + w b (and w = 1)
+    TFT_DEV W half(W x, W y, Tw<W> t, bool sel) const {
+        const W a = red2(x), b = mulw(y, t);
+        return sel ? a - b + p2 : a + b;
+    }
+    TFT_DEV W half1(W x, W y, bool sel) const {
+        const W a = red2(x), b = red2(y);
+        return sel ? a - b + p2 : a + b;
+    }
     // canonical-in/canonical-out helpers (cheap paths of the inverse solver)
     TFT_DEV W cadd(W a, W b) const { return red1(a + b); }
     TFT_DEV W csub(W a, W b) const { return red1(a - b + p); }
@@ -118,6 +127,11 @@ struct F32 {
         x = cadd(a, b);
         y = csub(a, b);
     }
+    TFT_DEV W half(W x, W y, Tw<W> t, bool sel) const {
+        const W b = mulw(y, t);
+        return sel ? csub(x, b) : cadd(x, b);
+    }
+    TFT_DEV W half1(W x, W y, bool sel) const { return sel ? csub(x, y) : cadd(x, y); }
     TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
         W s = cadd(x, y);
         W d = csub(x, y);
@@ -158,6 +172,14 @@ struct F62 {
         W d = x - y + p2;
         x = s;
         y = mulw(d, t);
+    }
+    TFT_DEV W half(W x, W y, Tw<W> t, bool sel) const {
+        const W a = red2(x), b = mulw(y, t);
+        return sel ? a - b + p2 : a + b;
+    }
+    TFT_DEV W half1(W x, W y, bool sel) const {
+        const W a = red2(x), b = red2(y);
+        return sel ? a - b + p2 : a + b;
     }
     TFT_DEV W cadd(W a, W b) const { return red1(a + b); }
     TFT_DEV W csub(W a, W b) const { return red1(a - b + p); }

@@ -47,7 +47,19 @@ struct LaunchArgs {
     W* stash;             // per-vector stash, C words each
     int l0, l1, wlog;     // two-pass plan (large kernels)
     int64_t vbase;        // first vector of this launch
+    unsigned long long* timing;  // debug: per-CTA phase timestamps (null in production)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TFTB_STAMP(a, k)                                                                                   \
+    do {                                                                                                   \
+        if ((a).timing && threadIdx.x == 0)                                                                \
+            (a).timing[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtime();                 \
+    } while (0)
 
 template <class F>
 TFT_DEV typename F::W load_pre(const LaunchArgs<F>& a, int64_t idx, typename F::W v) {
