@@ -123,11 +123,11 @@ TFT_DEV constexpr uint32_t unit_off(int i) {
 // Forward round.  With PRUNE, units whose every output row is >= lim are
 // skipped (only rows < lim are needed after the remaining stages).
 template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
-TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need) {
+TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t lim = PRUNE ? ((need + (1u << SLO) - 1) >> SLO) << SLO : 0;
-    for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
+    for (uint32_t g = ln.id; g < NU; g += ln.n) {
         const uint32_t col = g & ((1u << WLOG) - 1), u = g >> WLOG;
         const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
         if (PRUNE && base >= lim) continue;
@@ -147,11 +147,11 @@ TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t n
 // reg_inv); SCALE=false leaves an unmasked tile scaled by 2^TL.
 template <class F, int TL, int KK, int SLO, int WLOG, bool MASK, bool SCALE, class TP>
 TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
-                          uint32_t h) {
+                          uint32_t h, Lanes ln) {
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t h_lo = MASK ? (uint32_t)(((uint64_t)h >> (SLO + 1)) << (SLO + 1)) : 0;
-    for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
+    for (uint32_t g = ln.id; g < NU; g += ln.n) {
         const uint32_t col = g & ((1u << WLOG) - 1), u = g >> WLOG;
         const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
         if (MASK && base >= h_lo) continue;
@@ -169,28 +169,28 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
 // stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),
 // recursing down to a final 5-or-fewer-stage round at s_lo = 0.
 template <class F, int TL, int SHI, int WLOG = 0, bool PRUNE = false, class TP>
-TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need = 0) {
+TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need = 0, Lanes ln = cta_lanes()) {
     if constexpr (SHI <= 5) {
-        fwd_round_ct<F, TL, SHI, 0, WLOG, PRUNE>(f, S, tp, need);
+        fwd_round_ct<F, TL, SHI, 0, WLOG, PRUNE>(f, S, tp, need, ln);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        fwd_round_ct<F, TL, KK, SHI - KK, WLOG, PRUNE>(f, S, tp, need);
+        fwd_round_ct<F, TL, KK, SHI - KK, WLOG, PRUNE>(f, S, tp, need, ln);
         __syncthreads();
-        fwd_rounds_ct<F, TL, SHI - KK, WLOG, PRUNE>(f, S, tp, need);
+        fwd_rounds_ct<F, TL, SHI - KK, WLOG, PRUNE>(f, S, tp, need, ln);
     }
 }
 
 template <class F, int TL, int SHI, bool MASK, class TP, bool SCALE = true, int WLOG = 0>
 TFT_DEV void inv_rounds_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
-                           uint32_t h = 0) {
+                           uint32_t h = 0, Lanes ln = cta_lanes()) {
     if constexpr (SHI <= 5) {
-        inv_round_ct<F, TL, SHI, 0, WLOG, MASK, SCALE>(f, S, tp, ipow2, h);
+        inv_round_ct<F, TL, SHI, 0, WLOG, MASK, SCALE>(f, S, tp, ipow2, h, ln);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        inv_rounds_ct<F, TL, SHI - KK, MASK, TP, SCALE, WLOG>(f, S, tp, ipow2, h);
-        inv_round_ct<F, TL, KK, SHI - KK, WLOG, MASK, SCALE>(f, S, tp, ipow2, h);
+        inv_rounds_ct<F, TL, SHI - KK, MASK, TP, SCALE, WLOG>(f, S, tp, ipow2, h, ln);
+        inv_round_ct<F, TL, KK, SHI - KK, WLOG, MASK, SCALE>(f, S, tp, ipow2, h, ln);
         __syncthreads();
     }
 }
@@ -295,58 +295,114 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     TFTB_STAMP(a, 6);
 }
 
-// column solve: rows j < M of column `ph` (physical index) hold the column's
-// first M outputs; replace them by its M coefficients (V_M^-1, M^2 products);
-// optionally write the next output sum_j x_j omega_M^j into row M.
+// dot product of M canonical words with M Montgomery words, reduced once:
+// the raw 64-bit products accumulate exactly while their sum stays below
+// p 2^32 (<= 4 terms for p < 2^30), then one REDC gives the value
+TFT_DEV uint32_t redc_dot4(const F30& f, const uint32_t* y, const uint32_t* wM, int m) {
+    uint64_t acc = 0;
+#pragma unroll 4
+    for (int c = 0; c < 4; ++c)
+        if (c < m) acc += (uint64_t)y[c] * wM[c];
+    const uint32_t q = (uint32_t)acc * f.npinv;
+    return f.red1((uint32_t)((acc + (uint64_t)q * f.p) >> 32));
+}
+
+// column solve: y[0..M) are the column's first M outputs; xv <- its M
+// coefficients (V_M^-1, M^2 products, canonical) and, if wanted, nv <- the
+// next output sum_j x_j omega_M^j
 template <class F, int M>
-TFT_DEV void col_solve_vals(const F& f, typename F::W* const* rs, uint32_t ph, const typename F::W* yin,
-                            const Tw<typename F::W>* blk, bool write_next) {
+TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typename F::W>* blk,
+                            const typename F::W* blkM, typename F::W* xv, typename F::W* nv) {
     using W = typename F::W;
-    W y[M], xv[M];
+    W y[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) y[j] = f.canon(yin[j]);
+    if constexpr (std::is_same<F, F30>::value) {
+        // REDC dot products over raw Montgomery entries, <= 4 terms per reduction
 #pragma unroll
-    for (int r = 0; r < M; ++r) {
-        W acc = 0;
+        for (int r = 0; r < M; ++r) {
+            W acc = 0;
 #pragma unroll
-        for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(y[c], blk[8 * r + c]));
-        xv[r] = acc;
+            for (int c0 = 0; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, y + c0, blkM + 8 * r + c0, M - c0));
+            xv[r] = acc;
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            W acc = 0;
+#pragma unroll
+            for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(y[c], blk[8 * r + c]));
+            xv[r] = acc;
+        }
     }
-#pragma unroll
-    for (int r = 0; r < M; ++r) rs[r][ph] = xv[r];
-    if (write_next) {
+    if (nv) {
         W acc = 0;
+        if constexpr (std::is_same<F, F30>::value) {
 #pragma unroll
-        for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(xv[c], blk[64 + c]));
-        rs[M][ph] = acc;
+            for (int c0 = 0; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, xv + c0, blkM + 64 + c0, M - c0));
+        } else {
+#pragma unroll
+            for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(xv[c], blk[64 + c]));
+        }
+        *nv = acc;
     }
 }
 
+// solve columns [lo, hi): inputs are rows j < M of the cluster's tiles (DSMEM);
+// the M coefficients of a column are final outputs and go straight to the
+// vector in global memory (row r of column c is x[r C + c]; a warp's stores
+// are 32 consecutive words), only the next output crosses DSMEM, into row M
 template <class F, int M>
-TFT_DEV void col_solve_range(const F& f, typename F::W* const* rs, uint32_t lo, uint32_t hi,
-                             const Tw<typename F::W>* blk, bool write_next) {
+TFT_DEV void col_solve_range(const F& f, typename F::W* const* rs, typename F::W* xg, uint32_t C, uint32_t lo,
+                             uint32_t hi, const Tw<typename F::W>* blk, const typename F::W* blkM,
+                             bool write_next) {
     using W = typename F::W;
-    for (uint32_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    uint32_t c = lo + threadIdx.x;
+    auto one = [&](uint32_t cc, const W* y) {
+        const uint32_t ph = cc + (cc >> 5);
+        W xv[M], nv;
+        col_solve_vals<F, M>(f, y, blk, blkM, xv, write_next ? &nv : nullptr);
+#pragma unroll
+        for (int r = 0; r < M; ++r) xg[(size_t)r * C + cc] = xv[r];
+        if (write_next) rs[M][ph] = nv;
+    };
+    if constexpr (M <= 4) {
+        // two columns per thread: 2M remote loads in flight before any math
+        for (; c + blockDim.x < hi; c += 2 * blockDim.x) {
+            const uint32_t c1 = c + blockDim.x;
+            const uint32_t ph0 = c + (c >> 5), ph1 = c1 + (c1 >> 5);
+            W y0[M], y1[M];
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                y0[j] = rs[j][ph0];
+                y1[j] = rs[j][ph1];
+            }
+            one(c, y0);
+            one(c1, y1);
+        }
+    }
+    for (; c < hi; c += blockDim.x) {
         const uint32_t ph = c + (c >> 5);
         W y[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) y[j] = rs[j][ph];
-        col_solve_vals<F, M>(f, rs, ph, y, blk, write_next);
+        one(c, y);
     }
 }
 
 template <class F>
-TFT_DEV void col_solve(const F& f, typename F::W* const* rs, uint32_t lo, uint32_t hi, int m,
-                       const Tw<typename F::W>* blk, bool write_next) {
+TFT_DEV void col_solve(const F& f, typename F::W* const* rs, typename F::W* xg, uint32_t C, uint32_t lo,
+                       uint32_t hi, int m, const Tw<typename F::W>* blk, const typename F::W* blkM,
+                       bool write_next) {
     switch (m) {
-        case 1: col_solve_range<F, 1>(f, rs, lo, hi, blk, write_next); break;
-        case 2: col_solve_range<F, 2>(f, rs, lo, hi, blk, write_next); break;
-        case 3: col_solve_range<F, 3>(f, rs, lo, hi, blk, write_next); break;
-        case 4: col_solve_range<F, 4>(f, rs, lo, hi, blk, write_next); break;
-        case 5: col_solve_range<F, 5>(f, rs, lo, hi, blk, write_next); break;
-        case 6: col_solve_range<F, 6>(f, rs, lo, hi, blk, write_next); break;
-        case 7: col_solve_range<F, 7>(f, rs, lo, hi, blk, write_next); break;
-        default: col_solve_range<F, 8>(f, rs, lo, hi, blk, write_next); break;
+        case 1: col_solve_range<F, 1>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 2: col_solve_range<F, 2>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 3: col_solve_range<F, 3>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 4: col_solve_range<F, 4>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 5: col_solve_range<F, 5>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 6: col_solve_range<F, 6>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 7: col_solve_range<F, 7>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        default: col_solve_range<F, 8>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
     }
 }
 
@@ -365,46 +421,53 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     W* x = a.x + o;
     const F f = a.f;
     const int64_t cbase = (int64_t)g * C;
-
+    TFTB_STAMP(a, 0);
     if (a.pre)
         tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
     else
         tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
+    TFTB_STAMP(a, 1);
     // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
     // known outputs [0, h), never the tail the columns will fill) alongside
     const TwDirect<F> tpi{a.R.Zi, g, CL, f};
     // complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
     if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+    TFTB_STAMP(a, 2);
     cl.sync();
+    TFTB_STAMP(a, 3);
 
     W* rs[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
     {
+        // columns >= h: K known rows; their coefficients are final
         uint32_t lo, hi;
         col_share(h, C, g, G, lo, hi);
-        col_solve(f, rs, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1), h != 0);
+        col_solve(f, rs, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1), a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
     }
+    TFTB_STAMP(a, 4);
+    // (with h == 0 this is only the exit barrier: no CTA may leave while
+    // others still read its tile)
     cl.sync();
-    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
-    if (h && g == K) {
+    if (!h) return;
+    if (g == K) {
         SmemTile<W> tl{S, CL, 0};
         itft_phases23(f, tl, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
-    } else if (h) {
-        // columns >= h of this chunk are final: store them while chunk K is solved
-        for (uint32_t i = h + threadIdx.x; i < lim; i += blockDim.x) x[cbase + i] = f.canon(S[i + (i >> 5)]);
     }
+    TFTB_STAMP(a, 5);
     cl.sync();
-    if (h) {
+    {
+        // columns < h: K + 1 rows, the last from the solved chunk K
         uint32_t lo, hi;
         col_share(0, h, g, G, lo, hi);
-        col_solve(f, rs, lo, hi, (int)K + 1, a.R.vinvT + 72 * K, false);
+        col_solve(f, rs, x, C, lo, hi, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
     }
+    TFTB_STAMP(a, 6);
+    // no CTA may exit while others still read its tile
     cl.sync();
-    if (!h || g == K) tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
-    else tile_store<W>(x + cbase, S, h, [&](W w) { return f.canon(w); });
+    TFTB_STAMP(a, 7);
 }
 
 // ================================================ two-pass plan, chunk pass
@@ -691,7 +754,10 @@ __global__ void __launch_bounds__(256, 3) k_clg_fwd(LaunchArgs<F> a) {
                 for (int j = 0; j < GP; ++j) {
                     const int64_t pos = (int64_t)j * C + head + (int64_t)q * NV;
                     if (q < nq && pos + NV <= nin) {
-                        buf[u][j] = ld_stream(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
+                        // the vector's other CTAs read the same rows: keep them in L2
+                        buf[u][j] = __ldg(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
+                    } else if (pos >= nin) {
+                        buf[u][j] = Vec16<W>::zero();
                     } else {
                         W e[NV];
 #pragma unroll

@@ -59,7 +59,7 @@ extern "C" int tftb_debug_itft_tile(uint64_t p, uint64_t top, int K, void* data,
 // length n): out[cta*8 + k], k = 0 start, 1 loaded, 2 synced, 3 cross done,
 // 4 synced, 5 rounds done, 6 stored.
 extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* data, int64_t n, int64_t count,
-                                         unsigned long long* out) {
+                                         unsigned long long* out, int inverse) {
     using namespace tftb;
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
@@ -76,7 +76,7 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     a.timing = out;
     constexpr int CL = Limits<F30>::CL;
     const size_t smem = padded_words(1u << CL) * 4;
-    if (set_smem(k_cl_fwd<F30, CL>, smem)) return -1;
+    if (set_smem(k_cl_fwd<F30, CL>, smem) || set_smem(k_cl_inv<F30, CL>, smem)) return -1;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(pl.G, (unsigned)count, 1);
     lc.blockDim = dim3(256, 1, 1);
@@ -88,7 +88,8 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F30, CL>, a));
+    if (inverse) CK(cudaLaunchKernelEx(&lc, k_cl_inv<F30, CL>, a));
+    else CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F30, CL>, a));
     CK(cudaDeviceSynchronize());
     return 0;
 }

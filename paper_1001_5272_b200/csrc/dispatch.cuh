@@ -1,9 +1,44 @@
 // Batch planning and launches (instantiated once per field type).
 #pragma once
-#include "cluster.cuh"
+#include "small.cuh"
 #include "host.h"
 
 namespace tftb {
+
+// whole-vector tiles of one size class T = ceil_lg(n)
+template <class F, int T>
+int launch_tiles(LaunchArgs<F> a, int64_t count, bool inverse, cudaStream_t st) {
+    using SH = TileShape<T>;
+    const size_t smem = SH::smem(sizeof(typename F::W));
+    auto k = inverse ? k_tile_inv<F, T> : k_tile_fwd<F, T>;
+    if (set_smem(k, smem)) return -1;
+    const int64_t per = (int64_t)SH::VPB << 30;  // vectors per launch (grid.x < 2^31)
+    for (int64_t v0 = 0; v0 < count; v0 += per) {
+        a.vbase = v0;
+        const int64_t nv = std::min(count - v0, per);
+        const unsigned nb = (unsigned)((nv + SH::VPB - 1) / SH::VPB);
+        k<<<nb, 256, smem, st>>>(a, v0 + nv);
+        g_launches++;
+        CK(cudaGetLastError());
+    }
+    return 0;
+}
+
+template <class F>
+int run_tiles(LaunchArgs<F> a, int T, int64_t count, bool inverse, cudaStream_t st) {
+    static_assert(Limits<F>::CL <= 14, "tile instantiations stop at 2^14");
+    switch (T) {
+#define TFTB_TILE_CASE(t) \
+    case t:              \
+        if constexpr (t <= Limits<F>::CL) return launch_tiles<F, t>(a, count, inverse, st); \
+        break;
+        TFTB_TILE_CASE(0) TFTB_TILE_CASE(1) TFTB_TILE_CASE(2) TFTB_TILE_CASE(3) TFTB_TILE_CASE(4)
+        TFTB_TILE_CASE(5) TFTB_TILE_CASE(6) TFTB_TILE_CASE(7) TFTB_TILE_CASE(8) TFTB_TILE_CASE(9)
+        TFTB_TILE_CASE(10) TFTB_TILE_CASE(11) TFTB_TILE_CASE(12) TFTB_TILE_CASE(13) TFTB_TILE_CASE(14)
+#undef TFTB_TILE_CASE
+    }
+    return fail("tile size class out of range");
+}
 
 // One group of vectors that share a plan.
 template <class F>
@@ -65,24 +100,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         }
         return 0;
     }
-    if (pl.kind == kSmall) {
-        size_t smem = padded_words(1u << pl.l) * sizeof(W);
-        int nt = std::max(32, std::min(kNT, (1 << pl.l) / 16));
-        if (inverse) {
-            if (set_smem(k_small_inv<F>, smem)) return -1;
-        } else {
-            if (set_smem(k_small_fwd<F>, smem)) return -1;
-        }
-        for (int64_t v0 = 0; v0 < count; v0 += (1ll << 30)) {
-            a.vbase = v0;
-            unsigned nb = (unsigned)std::min<int64_t>(count - v0, 1ll << 30);
-            if (inverse) k_small_inv<F><<<nb, nt, smem, st>>>(a);
-            else k_small_fwd<F><<<nb, nt, smem, st>>>(a);
-            g_launches++;
-            CK(cudaGetLastError());
-        }
-        return 0;
-    }
+    if (pl.kind == kSmall) return run_tiles<F>(a, pl.l, count, inverse, st);
     const uint32_t C = 1u << pl.l1;
     const int64_t maxchunks = (maxn + C - 1) / C;
     const int64_t vchunk = 65535;

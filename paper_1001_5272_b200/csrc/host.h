@@ -113,7 +113,8 @@ enum PlanKind { kSmall = 0, kCluster = 1, kLarge = 2 };
 struct Plan {
     PlanKind kind;
     int l, l0, l1, wlog, G;
-    int key() const { return kind == kSmall ? -1 : (kind == kCluster ? 1000 + G : l); }
+    // small vectors group by tile size class, cluster ones by chunk count
+    int key() const { return kind == kSmall ? -100 + l : (kind == kCluster ? 1000 + G : l); }
 };
 
 template <class F>

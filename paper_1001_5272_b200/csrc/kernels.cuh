@@ -78,6 +78,7 @@ struct Vec16<uint32_t> {
     static constexpr int N = 4;
     TFT_DEV static uint32_t get(const T& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
     TFT_DEV static T make(const uint32_t* e) { return T{e[0], e[1], e[2], e[3]}; }
+    TFT_DEV static T zero() { return T{0, 0, 0, 0}; }
 };
 template <>
 struct Vec16<uint64_t> {
@@ -85,6 +86,7 @@ struct Vec16<uint64_t> {
     static constexpr int N = 2;
     TFT_DEV static uint64_t get(const T& v, int i) { return i == 0 ? v.x : v.y; }
     TFT_DEV static T make(const uint64_t* e) { return T{e[0], e[1]}; }
+    TFT_DEV static T zero() { return T{0, 0}; }
 };
 
 template <typename T>
@@ -94,19 +96,19 @@ TFT_DEV T ld_stream(const T* p) { return __ldcs(p); }  // read once: evict-first
 // with 16-byte loads for the aligned body and UNR of them in flight per thread
 // (a tile load is one HBM latency, not C/blockDim of them).
 template <typename W, int UNR = 8, class XF>
-TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& xf) {
+TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& xf, Lanes ln = cta_lanes()) {
     using V = Vec16<W>;
     constexpr int NV = V::N;
     const uint32_t mis = (uint32_t)(((uintptr_t)src & 15) / sizeof(W));
     const uint32_t head = min(C, (uint32_t)((NV - mis) % NV));
-    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
+    for (uint32_t i = ln.id; i < head; i += ln.n) S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
     const uint32_t nq = (C - head) / NV;
     const typename V::T* vs = reinterpret_cast<const typename V::T*>(src + head);
-    for (uint32_t k0 = threadIdx.x; k0 < nq; k0 += blockDim.x * UNR) {
+    for (uint32_t k0 = ln.id; k0 < nq; k0 += ln.n * UNR) {
         typename V::T buf[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint32_t k = k0 + u * blockDim.x;
+            const uint32_t k = k0 + u * ln.n;
             const int64_t i = head + (int64_t)k * NV;
             if (k < nq && i + NV <= avail) {
                 buf[u] = ld_stream(vs + k);
@@ -119,79 +121,39 @@ TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& 
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint32_t k = k0 + u * blockDim.x;
+            const uint32_t k = k0 + u * ln.n;
             if (k >= nq) break;
             const uint32_t i = head + k * NV;
 #pragma unroll
             for (int q = 0; q < NV; ++q) S[(i + q) + ((i + q) >> 5)] = xf(i + q, V::get(buf[u], q));
         }
     }
-    for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x)
+    for (uint32_t i = head + nq * NV + ln.id; i < C; i += ln.n)
         S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
 }
 
 // dst[i] = cv(S[phys(i)]) for i < lim, 16-byte stores for the aligned body
 template <typename W, class CV>
-TFT_DEV void tile_store(W* dst, const W* S, uint32_t lim, const CV& cv) {
+TFT_DEV void tile_store(W* dst, const W* S, uint32_t lim, const CV& cv, Lanes ln = cta_lanes()) {
     using V = Vec16<W>;
     constexpr int NV = V::N;
     const uint32_t mis = (uint32_t)(((uintptr_t)dst & 15) / sizeof(W));
     const uint32_t head = min(lim, (uint32_t)((NV - mis) % NV));
-    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[i] = cv(S[i + (i >> 5)]);
+    for (uint32_t i = ln.id; i < head; i += ln.n) dst[i] = cv(S[i + (i >> 5)]);
     const uint32_t nq = (lim - head) / NV;
     typename V::T* vd = reinterpret_cast<typename V::T*>(dst + head);
-    for (uint32_t k = threadIdx.x; k < nq; k += blockDim.x) {
+    for (uint32_t k = ln.id; k < nq; k += ln.n) {
         const uint32_t i = head + k * NV;
         W e[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) e[q] = cv(S[(i + q) + ((i + q) >> 5)]);
         __stcs(vd + k, V::make(e));
     }
-    for (uint32_t i = head + nq * NV + threadIdx.x; i < lim; i += blockDim.x) dst[i] = cv(S[i + (i >> 5)]);
+    for (uint32_t i = head + nq * NV + ln.id; i < lim; i += ln.n) dst[i] = cv(S[i + (i >> 5)]);
 }
 
 __device__ __forceinline__ int ceil_lg_dev(int64_t n) {
     return n <= 1 ? 0 : 64 - __clzll((unsigned long long)(n - 1));
-}
-
-// ------------------------------------------------------------ small: 1 CTA/vector
-template <class F>
-__global__ void k_small_fwd(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    W* S = reinterpret_cast<W*>(smem_raw);
-    const int64_t v = a.vbase + blockIdx.x;
-    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
-    const int t = ceil_lg_dev(n);
-    W* x = a.x + a.xd.o(v);
-    const W* in = a.in + a.ind.o(v);
-    SmemTile<W> tl{S, t, 0};
-    tile_load<W>(S, in, nin, 1u << t, [](uint32_t, W w) { return w; });
-    __syncthreads();
-    fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
-    const F f = a.f;
-    tile_store<W>(x, S, (uint32_t)n, [&](W w) { return f.canon(w); });
-}
-
-template <class F>
-__global__ void k_small_inv(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    W* S = reinterpret_cast<W*>(smem_raw);
-    const int64_t v = a.vbase + blockIdx.x;
-    const int64_t n = a.xd.n(v);
-    const int t = ceil_lg_dev(n);
-    const int64_t o = a.xd.o(v);
-    W* x = a.x + o;
-    SmemTile<W> tl{S, t, 0};
-    if (a.pre)
-        tile_load<W>(S, x, n, 1u << t, [&](uint32_t i, W w) { return load_pre(a, o + i, w); });
-    else
-        tile_load<W>(S, x, n, 1u << t, [](uint32_t, W w) { return w; });
-    __syncthreads();
-    itft_gen(a.f, tl, (uint32_t)n, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
-    const F f = a.f;
-    tile_store<W>(x, S, (uint32_t)n, [&](W w) { return f.canon(w); });
 }
 
 // ------------------------------------------------------------ two-pass, forward

@@ -129,6 +129,17 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
         }
     }
     for (int var = 0; var < 3; var++) host.insert(host.end(), blocks[var].begin(), blocks[var].end());
+    // the same 3 x 8 x 72 entries as raw Montgomery words (w R mod p), packed
+    // two per Tw slot, for the REDC dot products of the column solves
+    {
+        std::vector<W> raw;
+        for (int var = 0; var < 3; var++)
+            for (auto& t : blocks[var]) {
+                uint64_t w = tb.shoup ? (uint64_t)t.w : 0;  // normal form for Shoup fields
+                raw.push_back(tb.shoup ? (W)tb.to_m(w) : t.w);
+            }
+        for (size_t i = 0; i < raw.size(); i += 2) host.push_back(Tw<W>{raw[i], raw[i + 1]});
+    }
     size_t tw_bytes = host.size() * sizeof(Tw<W>);
     CK(cudaMalloc(&rh->dmem, tw_bytes));
     CK(cudaMemcpy(rh->dmem, host.data(), tw_bytes, cudaMemcpyHostToDevice));
@@ -141,6 +152,7 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     out->vinv = d + 2 * nz + 2 * nh + 64;
     out->vinvS = out->vinv + 8 * 72;
     out->vinvT = out->vinv + 16 * 72;
+    out->vinvM = reinterpret_cast<const W*>(out->vinv + 24 * 72);
     uint64_t R1 = tb.to_m(1);
     out->r2w = (W)tb.to_m(R1);  // R^2 mod p
     out->inv2 = tb.tw(inv2);

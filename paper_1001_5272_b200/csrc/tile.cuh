@@ -19,6 +19,13 @@
 #pragma once
 #include "field.cuh"
 
+// The threads that cooperate on one tile: the whole CTA by default, or a
+// slice of it when a CTA carries several small tiles (k_tile_*).
+struct Lanes {
+    uint32_t id, n;
+};
+__device__ __forceinline__ Lanes cta_lanes() { return Lanes{threadIdx.x, blockDim.x}; }
+
 template <typename W>
 struct SmemTile {
     W* S;
@@ -42,6 +49,7 @@ struct RingDev {
     const Tw<W>* vinv;  // 8 blocks of 72: V_m^-1 (m x m, V_m[s][i] = omega_s^i), then omega_m^i
     const Tw<W>* vinvS; // same with every column times 2^-CL
     const Tw<W>* vinvT; // same with all but the last column times 2^-CL
+    const W* vinvM;     // vinv, vinvS, vinvT as raw Montgomery words (3 x 8 x 72)
     Tw<W> inv2;         // 1/2
     W r2w;              // R^2 mod p as a raw word: mont(mont(a, b), r2w) = a b
     W oneW;             // 1 as a field word (1, or R mod p for Montgomery fields)
@@ -269,59 +277,70 @@ TFT_DEV void inv_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp
 // inverse map is unique; the odd-tail Horner passes are not needed.
 template <class F, class TPF, class TPI>
 TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
-                      const TPI& tpi, const RingDev<typename F::W>& R) {
+                      const TPI& tpi, const RingDev<typename F::W>& R, Lanes ln = cta_lanes(),
+                      bool uniform = false) {
     using W = typename F::W;
     const int t = tl.t;
     const uint32_t ncols = 1u << tl.wlog;
-    if (h == 0 || h >= (1u << t)) return;
-    const int dlo = __ffs(h);  // levels d with h mod 2^d != 0
+    // uniform: every tile of the CTA walks all levels (the barriers must
+    // match); tiles with nothing to do at a level just skip its work
+    const bool act = h != 0 && h < (1u << t);
+    if (!uniform && !act) return;
+    const int dact = act ? __ffs(h) : t + 1;  // levels d with h mod 2^d != 0
+    const int dlo = uniform ? 1 : dact;
+    // (one barrier per level at a convergent point: with several tiles per
+    // warp, lanes of one warp may be active at different levels)
     for (int d = t; d >= dlo; --d) {
-        const uint32_t hd = h & ((1u << d) - 1);
-        const uint32_t B = h - hd, H = 1u << (d - 1);
-        const Tw<W> w = tpf.get(d - 1, B >> d);
-        if (hd >= H) {
-            const uint32_t i0 = hd - H, cnt = (H - i0) << tl.wlog;
-            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
-                uint32_t col = g & (ncols - 1), i = i0 + (g >> tl.wlog);
-                W tv = tl.at(tl.ix(B + H + i, col));
-                W lo = f.canon(tl.at(tl.ix(B + i, col)));
-                W m = f.cmulw(tv, w);
-                W x = f.csub(lo, m);
-                tl.at(tl.ix(B + i, col)) = x;
-                tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
-            }
-        } else {
-            const uint32_t cnt = (H - hd) << tl.wlog;
-            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
-                uint32_t col = g & (ncols - 1), i = hd + (g >> tl.wlog);
-                W a = tl.at(tl.ix(B + i, col));
-                W b = tl.at(tl.ix(B + H + i, col));
-                tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
+        if (d >= dact) {
+            const uint32_t hd = h & ((1u << d) - 1);
+            const uint32_t B = h - hd, H = 1u << (d - 1);
+            const Tw<W> w = tpf.get(d - 1, B >> d);
+            if (hd >= H) {
+                const uint32_t i0 = hd - H, cnt = (H - i0) << tl.wlog;
+                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
+                    uint32_t col = g & (ncols - 1), i = i0 + (g >> tl.wlog);
+                    W tv = tl.at(tl.ix(B + H + i, col));
+                    W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                    W m = f.cmulw(tv, w);
+                    W x = f.csub(lo, m);
+                    tl.at(tl.ix(B + i, col)) = x;
+                    tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
+                }
+            } else {
+                const uint32_t cnt = (H - hd) << tl.wlog;
+                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
+                    uint32_t col = g & (ncols - 1), i = hd + (g >> tl.wlog);
+                    W a = tl.at(tl.ix(B + i, col));
+                    W b = tl.at(tl.ix(B + H + i, col));
+                    tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
+                }
             }
         }
         __syncthreads();
     }
     for (int d = dlo; d <= t; ++d) {
-        const uint32_t hd = h & ((1u << d) - 1);
-        const uint32_t B = h - hd, H = 1u << (d - 1);
-        if (hd >= H) {
-            const Tw<W> wi = tpi.get(d - 1, B >> d);
-            const uint32_t cnt = (hd - H) << tl.wlog;
-            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
-                uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
-                W lo = f.canon(tl.at(tl.ix(B + i, col)));
-                W hi = tl.at(tl.ix(B + H + i, col));
-                tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), wi), R.inv2);
-            }
-        } else {
-            const Tw<W> w = tpf.get(d - 1, B >> d);
-            const uint32_t cnt = hd << tl.wlog;
-            for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
-                uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
-                W a = tl.at(tl.ix(B + i, col));
-                W b = tl.at(tl.ix(B + H + i, col));
-                tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
+        if (d >= dact) {
+            const uint32_t hd = h & ((1u << d) - 1);
+            const uint32_t B = h - hd, H = 1u << (d - 1);
+            if (hd >= H) {
+                const Tw<W> wi = tpi.get(d - 1, B >> d);
+                const uint32_t cnt = (hd - H) << tl.wlog;
+                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
+                    uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
+                    W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                    W hi = tl.at(tl.ix(B + H + i, col));
+                    tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
+                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), wi), R.inv2);
+                }
+            } else {
+                const Tw<W> w = tpf.get(d - 1, B >> d);
+                const uint32_t cnt = hd << tl.wlog;
+                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
+                    uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
+                    W a = tl.at(tl.ix(B + i, col));
+                    W b = tl.at(tl.ix(B + H + i, col));
+                    tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
+                }
             }
         }
         __syncthreads();

@@ -230,3 +230,29 @@ def test_host_batch_pipeline_against_oracle():
     assert np.array_equal(x, O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K))
     backend.check(lib.tftb_tft_batch_u64(x.ctypes.data, None, lp, lens.size, cfg.p, cfg.omegaK, cfg.K, 1))
     assert np.array_equal(x, flat)
+
+
+@pytest.mark.parametrize("key", ["p998244353", "p3221225473", "p4179340454199820289"])
+def test_shared_cta_small_tiles_against_oracle(golden, key):
+    """Many short vectors of one size class share a CTA (k_tile_*): ragged
+    lengths inside each class, partly-filled last CTA, both directions."""
+    cfg = cfg_for(golden, key)
+    rng = np.random.default_rng(31)
+    lens = np.concatenate([rng.integers(1, 33, 300), rng.integers(33, 257, 300),
+                           rng.integers(257, 4097, 61), [1, 2, 3, 32, 33, 4096]])
+    rng.shuffle(lens)
+    flat = rng.integers(0, cfg.p, int(lens.sum()), dtype=np.uint64)
+    d = device.to_words(flat, cfg)
+    device.tft_batch_(d, cfg, lengths=lens)
+    assert np.array_equal(device.from_words(d, cfg), O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K))
+    device.tft_batch_(d, cfg, lengths=lens, inverse=True)
+    assert np.array_equal(device.from_words(d, cfg), flat)
+    for la, lb, cnt in ((7, 5, 33), (100, 29, 9)):
+        a = rng.integers(0, cfg.p, cnt * la, dtype=np.uint64)
+        b = rng.integers(0, cfg.p, cnt * lb, dtype=np.uint64)
+        x = torch.zeros(cnt * (la + lb - 1), dtype=device.word_dtype(cfg), device="cuda")
+        device.multiply_batch(device.to_words(a, cfg), device.to_words(b, cfg), x, cfg, cnt, la, lb)
+        got = device.from_words(x, cfg).reshape(cnt, -1)
+        for v in range(cnt):
+            assert np.array_equal(got[v], O.multiply(a[v * la:(v + 1) * la], b[v * lb:(v + 1) * lb],
+                                                     cfg.p, cfg.omegaK, cfg.K)), (la, lb, v)
