@@ -151,6 +151,8 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t h_lo = MASK ? (uint32_t)(((uint64_t)h >> (SLO + 1)) << (SLO + 1)) : 0;
+    const uint32_t h_top = MASK ? (uint32_t)(((uint64_t)h >> (SLO + KK)) << (SLO + KK)) : 0;
+    const uint32_t h_top1 = MASK ? (uint32_t)(((uint64_t)h >> (SLO + KK + 1)) << (SLO + KK + 1)) : 0;
     for (uint32_t g = ln.id; g < NU; g += ln.n) {
         const uint32_t col = g & ((1u << WLOG) - 1), u = g >> WLOG;
         const uint32_t base = (u & ((1u << SLO) - 1)) | ((u >> SLO) << (SLO + KK));
@@ -160,7 +162,20 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
         W v[1 << KK];
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];
-        reg_inv<F, KK, 0, MASK>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
+        if constexpr (MASK) {
+            // a unit whose aligned 2^(SLO+KK) block lies below the top stage's
+            // bound is unmasked at every stage of the round; it is scaled (at
+            // the top stage only) when its block closes a complete block of [0, h)
+            constexpr int STOP = SLO + KK - 1;
+            const uint32_t blo = (base >> (STOP + 1)) << (STOP + 1), bhi = blo + (1u << (STOP + 1));
+            if (bhi <= h_top) {
+                reg_inv<F, KK, 0, false>(f, v, base, SLO, tp, h, blo >= h_top1 ? STOP : -1, ipow2);
+            } else {
+                reg_inv<F, KK, 0, true>(f, v, base, SLO, tp, h, -1, ipow2);
+            }
+        } else {
+            reg_inv<F, KK, 0, false>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
+        }
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
     }
@@ -348,61 +363,59 @@ TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typen
     }
 }
 
-// solve columns [lo, hi): inputs are rows j < M of the cluster's tiles (DSMEM);
-// the M coefficients of a column are final outputs and go straight to the
-// vector in global memory (row r of column c is x[r C + c]; a warp's stores
-// are 32 consecutive words), only the next output crosses DSMEM, into row M
-template <class F, int M>
-TFT_DEV void col_solve_range(const F& f, typename F::W* const* rs, typename F::W* xg, uint32_t C, uint32_t lo,
+// solve columns [lo, hi): ld(j, c) gives row j < M of column c (DSMEM or
+// global); the M coefficients of a column are final outputs and go straight
+// to the vector in global memory (row r of column c is x[r C + c]; a warp's
+// stores are 32 consecutive words); with write_next the next output goes to
+// nx(c, value)
+template <class F, int M, class LD, class NX>
+TFT_DEV void col_solve_range(const F& f, const LD& ld, const NX& nx, typename F::W* xg, uint32_t C, uint32_t lo,
                              uint32_t hi, const Tw<typename F::W>* blk, const typename F::W* blkM,
                              bool write_next) {
     using W = typename F::W;
     uint32_t c = lo + threadIdx.x;
     auto one = [&](uint32_t cc, const W* y) {
-        const uint32_t ph = cc + (cc >> 5);
         W xv[M], nv;
         col_solve_vals<F, M>(f, y, blk, blkM, xv, write_next ? &nv : nullptr);
 #pragma unroll
         for (int r = 0; r < M; ++r) xg[(size_t)r * C + cc] = xv[r];
-        if (write_next) rs[M][ph] = nv;
+        if (write_next) nx(cc, nv);
     };
     if constexpr (M <= 4) {
-        // two columns per thread: 2M remote loads in flight before any math
+        // two columns per thread: 2M loads in flight before any math
         for (; c + blockDim.x < hi; c += 2 * blockDim.x) {
             const uint32_t c1 = c + blockDim.x;
-            const uint32_t ph0 = c + (c >> 5), ph1 = c1 + (c1 >> 5);
             W y0[M], y1[M];
 #pragma unroll
             for (int j = 0; j < M; ++j) {
-                y0[j] = rs[j][ph0];
-                y1[j] = rs[j][ph1];
+                y0[j] = ld(j, c);
+                y1[j] = ld(j, c1);
             }
             one(c, y0);
             one(c1, y1);
         }
     }
     for (; c < hi; c += blockDim.x) {
-        const uint32_t ph = c + (c >> 5);
         W y[M];
 #pragma unroll
-        for (int j = 0; j < M; ++j) y[j] = rs[j][ph];
+        for (int j = 0; j < M; ++j) y[j] = ld(j, c);
         one(c, y);
     }
 }
 
-template <class F>
-TFT_DEV void col_solve(const F& f, typename F::W* const* rs, typename F::W* xg, uint32_t C, uint32_t lo,
+template <class F, class LD, class NX>
+TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg, uint32_t C, uint32_t lo,
                        uint32_t hi, int m, const Tw<typename F::W>* blk, const typename F::W* blkM,
                        bool write_next) {
     switch (m) {
-        case 1: col_solve_range<F, 1>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 2: col_solve_range<F, 2>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 3: col_solve_range<F, 3>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 4: col_solve_range<F, 4>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 5: col_solve_range<F, 5>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 6: col_solve_range<F, 6>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 7: col_solve_range<F, 7>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
-        default: col_solve_range<F, 8>(f, rs, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 1: col_solve_range<F, 1>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 2: col_solve_range<F, 2>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 3: col_solve_range<F, 3>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 4: col_solve_range<F, 4>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 5: col_solve_range<F, 5>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 6: col_solve_range<F, 6>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        case 7: col_solve_range<F, 7>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
+        default: col_solve_range<F, 8>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
     }
 }
 
@@ -442,31 +455,34 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
 #pragma unroll
     for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
     {
-        // columns >= h: K known rows; their coefficients are final
+        // columns >= h: K known rows; their coefficients are final, the next
+        // output of each goes into the last chunk's tile
         uint32_t lo, hi;
         col_share(h, C, g, G, lo, hi);
-        col_solve(f, rs, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1), a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
+        col_solve(
+            f, [&](int j, uint32_t c) { return rs[j][c + (c >> 5)]; },
+            [&](uint32_t c, W w) { rs[K][c + (c >> 5)] = w; }, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1),
+            a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
     }
+    // a complete chunk's columns < h are final after step 1: publish them for
+    // the last CTA's second solve (read back from L2), then leave -- the last
+    // chunk's solve below needs nobody else's tile
+    if (h && g < K)
+        for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
     TFTB_STAMP(a, 4);
-    // (with h == 0 this is only the exit barrier: no CTA may leave while
-    // others still read its tile)
+    // (also the exit barrier: no CTA may leave while others still read its tile)
     cl.sync();
-    if (!h) return;
-    if (g == K) {
+    if (!h || g != K) return;
+    TFTB_STAMP(a, 5);
+    {
         SmemTile<W> tl{S, CL, 0};
         itft_phases23(f, tl, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
     }
-    TFTB_STAMP(a, 5);
-    cl.sync();
-    {
-        // columns < h: K + 1 rows, the last from the solved chunk K
-        uint32_t lo, hi;
-        col_share(0, h, g, G, lo, hi);
-        col_solve(f, rs, x, C, lo, hi, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
-    }
     TFTB_STAMP(a, 6);
-    // no CTA may exit while others still read its tile
-    cl.sync();
+    // columns < h: K + 1 rows, K of them from the complete chunks
+    col_solve(
+        f, [&](int j, uint32_t c) { return (uint32_t)j < K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; },
+        [](uint32_t, W) {}, x, C, 0, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
     TFTB_STAMP(a, 7);
 }
 

@@ -122,7 +122,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         colf = k_colc_fwd<F, L>;        \
         coli = k_colc_inv<F, L>;        \
         break;
-        TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
+        TFTB_COL(1) TFTB_COL(2) TFTB_COL(3) TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
         TFTB_COL(10) TFTB_COL(11) TFTB_COL(12) TFTB_COL(13) TFTB_COL(14)
 #undef TFTB_COL
         default: return fail("no column kernel for this plan");

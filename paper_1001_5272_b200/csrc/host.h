@@ -128,7 +128,8 @@ int make_plan(int64_t n, Plan* pl) {
         pl->kind = kSmall;
         return 0;
     }
-    if (n <= (8ll << CL)) {
+    static const bool no_cluster = getenv("TFTB_NO_CLUSTER") != nullptr;  // A/B knob
+    if (n <= (8ll << CL) && !no_cluster) {
         pl->kind = kCluster;
         pl->G = (int)((n + (1ll << CL) - 1) >> CL);
         return 0;

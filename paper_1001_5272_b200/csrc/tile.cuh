@@ -289,12 +289,25 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
     const int dact = act ? __ffs(h) : t + 1;  // levels d with h mod 2^d != 0
     const int dlo = uniform ? 1 : dact;
     // (one barrier per level at a convergent point: with several tiles per
-    // warp, lanes of one warp may be active at different levels)
+    // warp, lanes of one warp may be active at different levels).  Each
+    // level's twiddle is fetched one level ahead so its global-memory latency
+    // overlaps the previous level instead of sitting between two barriers.
+    auto tw2 = [&](int d) {  // phase-2 twiddle of level d
+        const uint32_t B = h - (h & ((1u << d) - 1));
+        return tpf.get(d - 1, B >> d);
+    };
+    auto tw3 = [&](int d) {  // phase-3 twiddle of level d
+        const uint32_t hd = h & ((1u << d) - 1), B = h - hd;
+        return hd >= (1u << (d - 1)) ? tpi.get(d - 1, B >> d) : tpf.get(d - 1, B >> d);
+    };
+    Tw<W> wn = act && t >= dact ? tw2(t) : Tw<W>{};
+    Tw<W> wn3 = act && dact <= t ? tw3(dact) : Tw<W>{};
     for (int d = t; d >= dlo; --d) {
+        const Tw<W> w = wn;
+        if (act && d - 1 >= dact) wn = tw2(d - 1);
         if (d >= dact) {
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
-            const Tw<W> w = tpf.get(d - 1, B >> d);
             if (hd >= H) {
                 const uint32_t i0 = hd - H, cnt = (H - i0) << tl.wlog;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
@@ -319,21 +332,21 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
         __syncthreads();
     }
     for (int d = dlo; d <= t; ++d) {
+        const Tw<W> w = wn3;
+        if (act && d >= dact && d + 1 <= t) wn3 = tw3(d + 1);
         if (d >= dact) {
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
             if (hd >= H) {
-                const Tw<W> wi = tpi.get(d - 1, B >> d);
                 const uint32_t cnt = (hd - H) << tl.wlog;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
                     uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
                     W lo = f.canon(tl.at(tl.ix(B + i, col)));
                     W hi = tl.at(tl.ix(B + H + i, col));
                     tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), wi), R.inv2);
+                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), w), R.inv2);
                 }
             } else {
-                const Tw<W> w = tpf.get(d - 1, B >> d);
                 const uint32_t cnt = hd << tl.wlog;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
                     uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
