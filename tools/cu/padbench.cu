@@ -1,0 +1,108 @@
+// Round throughput vs shared-memory row padding: P = 1 word per 32 (scalar
+// accesses everywhere) against P = 4 words (16 B; the SLO = 0 round moves
+// its 32-word units with 128-bit LDS/STS).  F30, 2^14-word tile, rounds
+// (5 @ 9), (4 @ 5), (5 @ 0) repeated.
+#include <cstdio>
+#include <vector>
+#include "../../paper_1001_5272_b200/csrc/cluster.cuh"
+
+// twiddle provider whose indices stay inside a 64-entry (L1-resident) window:
+// same instruction stream, no L2 traffic (numerically meaningless)
+struct TwSmall {
+    const Tw<uint32_t>* Z;
+    TFT_DEV Tw<uint32_t> get(int, uint32_t J) const { return ldg_tw(Z + (J & 63)); }
+    template <int N>
+    TFT_DEV void get_many(int, uint32_t J0, Tw<uint32_t>* out) const {
+        ldg_tw_run<uint32_t, N>(Z + (J0 & 63 & ~(N - 1)), out);
+    }
+};
+
+struct TwBcast {  // every thread reads the same twiddles (broadcast)
+    const Tw<uint32_t>* Z;
+    TFT_DEV Tw<uint32_t> get(int, uint32_t J) const { return ldg_tw(Z); }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t, Tw<uint32_t>* out) const { ldg_tw_run<uint32_t, N>(Z + 32 * s, out); }
+};
+
+template <int P, int KK, int SLO, class TP>
+__device__ __forceinline__ void round_p(const F30& f, uint32_t* S, const TP& tp) {
+    constexpr uint32_t NU = 1u << (14 - KK);
+    constexpr uint32_t STEP = SLO >= 5 ? (1u << SLO) + (P << (SLO - 5)) : 1u;
+    for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
+        const uint32_t base = (g & ((1u << SLO) - 1)) | ((g >> SLO) << (SLO + KK));
+        uint32_t* pb = S + base + (base >> 5) * P;
+        uint32_t v[1 << KK];
+        if constexpr (SLO == 0 && KK == 5 && P == 4) {
+            const uint4* pv = reinterpret_cast<const uint4*>(pb);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint4 t = pv[q];
+                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
+        }
+        reg_fwd<F30, KK, KK - 1>(f, v, base, SLO, tp);
+        if constexpr (SLO == 0 && KK == 5 && P == 4) {
+            uint4* pv = reinterpret_cast<uint4*>(pb);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pv[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < (1 << KK); ++i) pb[i * STEP] = v[i];
+        }
+    }
+}
+
+template <int P, int SMALL>
+__global__ void __launch_bounds__(256, 3) kround(F30 f, const Tw<uint32_t>* Z, uint32_t* out, int reps) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
+    for (uint32_t i = threadIdx.x; i < 16384; i += blockDim.x) S[i + (i >> 5) * P] = i * 2654435761u % f.p;
+    __syncthreads();
+    const TwDirect<F30> tp{Z, blockIdx.x & 3, 14, f};
+    for (int r = 0; r < reps; ++r) {
+        round_p<P, 5, 9>(f, S, tp);
+        __syncthreads();
+        round_p<P, 4, 5>(f, S, tp);
+        __syncthreads();
+        if constexpr (SMALL == 2) round_p<P, 5, 0>(f, S, TwBcast{Z});
+        else if constexpr (SMALL == 1) round_p<P, 5, 0>(f, S, TwSmall{Z});
+        else round_p<P, 5, 0>(f, S, tp);
+        __syncthreads();
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = S[threadIdx.x];
+}
+
+template <int P, int SMALL>
+void run(F30 f, Tw<uint32_t>* Z, uint32_t* out) {
+    size_t smem = (16384 + 512 * P + P) * 4;
+    cudaFuncSetAttribute(kround<P, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    int reps = 40, grid = 148 * 3 * 4;
+    for (int k = 0; k < 3; ++k) {
+        cudaEventRecord(a);
+        kround<P, SMALL><<<grid, 256, smem>>>(f, Z, out, reps);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        double bf = (double)grid * reps * 14 * 8192;
+        if (k) printf("small=%d P=%d: %.3f ms, %.2f butterflies/clk/SM @1.965GHz (%s)\n", (int)SMALL, P, ms, bf / (ms * 1e-3) / 148 / 1.965e9,
+                      cudaGetErrorString(cudaGetLastError()));
+    }
+}
+
+int main() {
+    const uint32_t p = 998244353u;
+    F30 f;
+    f.p = p; f.p2 = 2 * p;
+    uint32_t x = p; for (int i = 0; i < 6; ++i) x *= 2u - p * x;
+    f.pinv = x; f.npinv = 0u - x; f.c32 = (uint32_t)((1ull << 32) % p); f.c32s = (uint32_t)(((unsigned __int128)f.c32 << 32) / p);
+    std::vector<Tw<uint32_t>> h(1 << 16);
+    for (size_t j = 0; j < h.size(); ++j) { uint32_t w = (uint32_t)((j * 7919ull + 1) % p); h[j] = {w, (uint32_t)(((unsigned __int128)w << 32) / p)}; }
+    Tw<uint32_t>* Z; cudaMalloc(&Z, h.size() * 8); cudaMemcpy(Z, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    uint32_t* out; cudaMalloc(&out, 148 * 3 * 4 * 256 * 4);
+    run<1, 0>(f, Z, out);
+    run<1, 1>(f, Z, out);
+    run<1, 2>(f, Z, out);
+}
