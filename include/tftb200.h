@@ -109,6 +109,14 @@ const char* tftb_version(void);
 /* Number of kernel launches issued by this thread since the last reset. */
 int64_t tftb_launch_count(int reset);
 
+/* ------------------------------------------------------------ op tallies
+ * (mults, adds) the reference walk reports for the same call: the second
+ * tuple element of _kernels.tft / _kernels.itft (_kernels.pyx:415-430) and
+ * of _kernels.multiply (_kernels.pyx:433-480).  Host-only (no GPU needed);
+ * tftb_tft_u64 / tftb_itft_u64 / tftb_multiply_u64 return the same values. */
+int tftb_tally_transform(int64_t n, uint64_t p, int K, int inverse, int64_t* mults, int64_t* adds);
+int tftb_tally_multiply(int64_t la, int64_t lb, uint64_t p, int K, int64_t* mults, int64_t* adds);
+
 #ifdef __cplusplus
 }
 #endif

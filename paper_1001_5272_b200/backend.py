@@ -59,6 +59,9 @@ SIGNATURES = {
     "tftb_last_error": (ctypes.c_char_p, []),
     "tftb_version": (ctypes.c_char_p, []),
     "tftb_launch_count": (ctypes.c_int64, [ctypes.c_int]),
+    "tftb_tally_transform": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _i64p, _i64p]),
+    "tftb_tally_multiply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, _i64p,
+                                           _i64p]),
 }
 
 _lib = None

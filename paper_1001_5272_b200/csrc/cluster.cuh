@@ -381,19 +381,16 @@ TFT_DEV void col_solve_range(const F& f, const LD& ld, const NX& nx, typename F:
         for (int r = 0; r < M; ++r) xg[(size_t)r * C + cc] = xv[r];
         if (write_next) nx(cc, nv);
     };
-    if constexpr (M <= 4) {
-        // two columns per thread: 2M loads in flight before any math
-        for (; c + blockDim.x < hi; c += 2 * blockDim.x) {
-            const uint32_t c1 = c + blockDim.x;
-            W y0[M], y1[M];
+    // CIF columns per thread: CIF*M loads in flight before any math
+    constexpr int CIF = M <= 2 ? 8 : (M <= 4 ? 4 : 2);
+    for (; c + (CIF - 1) * blockDim.x < hi; c += CIF * blockDim.x) {
+        W y[CIF][M];
 #pragma unroll
-            for (int j = 0; j < M; ++j) {
-                y0[j] = ld(j, c);
-                y1[j] = ld(j, c1);
-            }
-            one(c, y0);
-            one(c1, y1);
-        }
+        for (int k = 0; k < CIF; ++k)
+#pragma unroll
+            for (int j = 0; j < M; ++j) y[k][j] = ld(j, c + k * blockDim.x);
+#pragma unroll
+        for (int k = 0; k < CIF; ++k) one(c + k * blockDim.x, y[k]);
     }
     for (; c < hi; c += blockDim.x) {
         W y[M];

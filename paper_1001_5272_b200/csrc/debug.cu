@@ -88,8 +88,18 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    if (inverse) CK(cudaLaunchKernelEx(&lc, k_cl_inv<F30, CL>, a));
-    else CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F30, CL>, a));
+    if (inverse == 2) {  // the no-cluster forward the dispatcher uses
+        const int gam = pl.l - CL;
+        void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
+                                     : gam == 2 ? k_clg_fwd<F30, CL, 2> : k_clg_fwd<F30, CL, 3>;
+        if (set_smem(kg, smem)) return -1;
+        kg<<<dim3(pl.G, (unsigned)count, 1), 256, smem>>>(a);
+        CK(cudaGetLastError());
+    } else if (inverse) {
+        CK(cudaLaunchKernelEx(&lc, k_cl_inv<F30, CL>, a));
+    } else {
+        CK(cudaLaunchKernelEx(&lc, k_cl_fwd<F30, CL>, a));
+    }
     CK(cudaDeviceSynchronize());
     return 0;
 }

@@ -16,6 +16,7 @@
 #include "../../include/tftb200.h"
 #include "host.h"
 #include "kernels.cuh"
+#include "tally.h"
 
 namespace tftb {
 
@@ -206,14 +207,6 @@ int get_ring(uint64_t p, uint64_t top, int K, RingHost** out) {
 }
 
 // model op counts of the device algorithm
-void model_counts(int64_t n, bool inverse, int64_t* mults, int64_t* adds) {
-    int l = ceil_lg(n);
-    int64_t N = (int64_t)1 << l;
-    int64_t bf = (N / 2) * l;
-    if (mults) *mults = inverse ? bf + n : bf;
-    if (adds) *adds = 2 * bf;
-}
-
 int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, bool inverse, int64_t* mults,
                     int64_t* adds) {
     if (n <= 0) return fail("cannot transform an empty buffer");
@@ -242,7 +235,7 @@ int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, boo
     }
     CK(cudaMemcpyAsync(x, d64, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    model_counts(n, inverse, mults, adds);
+    tally_transform(n, p, K, inverse, mults, adds);
     return 0;
 }
 
@@ -303,11 +296,7 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     }
     CK(cudaMemcpyAsync(x, dx64, (size_t)r * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int64_t m1, a1, m2, a2;
-    model_counts(r, false, &m1, &a1);
-    model_counts(r, true, &m2, &a2);
-    if (mults) *mults = 2 * m1 + m2 + r;
-    if (adds) *adds = 2 * a1 + a2;
+    tally_multiply(la, lb, p, K, mults, adds);
     return 0;
 }
 
@@ -553,6 +542,18 @@ int64_t tftb_launch_count(int reset) {
     int64_t v = g_launches;
     if (reset) g_launches = 0;
     return v;
+}
+
+int tftb_tally_transform(int64_t n, uint64_t p, int K, int inverse, int64_t* mults, int64_t* adds) {
+    if (n <= 0) return fail("cannot tally an empty transform");
+    tally_transform(n, p, K, inverse != 0, mults, adds);
+    return 0;
+}
+
+int tftb_tally_multiply(int64_t la, int64_t lb, uint64_t p, int K, int64_t* mults, int64_t* adds) {
+    if (la <= 0 || lb <= 0) return fail("cannot tally an empty product");
+    tally_multiply(la, lb, p, K, mults, adds);
+    return 0;
 }
 
 }  // extern "C"

@@ -3,7 +3,8 @@
 Run in the build container (where /root/reference exists):
 
     make -C oracle ref            # the reference's compiled kernels -> oracle/_ref
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # golden.json and tallies.json
+    python tests/golden/make_golden.py --tallies  # tallies.json only
 
 Two sources, both the reference's own code:
   * the public pure-Python API of `tftmul` imported from
@@ -190,5 +191,44 @@ def main():
     print(f"wrote golden.json in {time.time() - t0:.1f}s")
 
 
+def tallies():
+    """tests/golden/tallies.json: the (mults, adds) the reference's compiled
+    kernels return (`_kernels.pyx:415-480`) -- value-independent, so zeros in."""
+    t0 = time.time()
+    out = {"transforms": [], "products": []}
+    sizes = {
+        "p17": list(range(1, 17)),
+        "p998244353": list(range(1, 301)) + [1000, 1023, 1024, 1025, 8191, 8193, 16385, 32772, 49153,
+                                             54613, 65530, 65537, 131073, 1 << 22, (1 << 22) + 1,
+                                             3 << 21, (1 << 23) - 1, 1 << 23],
+        "p3221225473": [1, 2, 3, 100, 65537, (1 << 20) + 1, 3 << 19],
+        "p4179340454199820289": [1, 2, 3, 100, 65537, 300001],
+    }
+    for key, lens in sizes.items():
+        p, top, K = PRIMES[key]
+        for n in lens:
+            z = array("Q", bytes(8 * n))
+            fm, fa = K_.tft(memoryview(z), 0, n, p, top, K)
+            im, ia = K_.itft(memoryview(z), 0, n, p, top, K, (p + 1) >> 1)
+            out["transforms"].append({"prime": key, "n": n, "tft": [fm, fa], "itft": [im, ia]})
+        print(f"tallies {key} ({time.time() - t0:.1f}s)", flush=True)
+    for key, la, lb in (("p17", 1, 1), ("p17", 2, 3), ("p17", 5, 9), ("p998244353", 1, 1000),
+                        ("p998244353", 64, 64), ("p998244353", 100, 29), ("p998244353", 3001, 1999),
+                        ("p998244353", 65536, 65537), ("p998244353", 2500001, 1750004),
+                        ("p3221225473", 40000, 30001), ("p4179340454199820289", 20000, 12345)):
+        p, top, K = PRIMES[key]
+        A, B = array("Q", bytes(8 * la)), array("Q", bytes(8 * lb))
+        X = array("Q", bytes(8 * (la + lb - 1)))
+        m, a = K_.multiply(memoryview(A), memoryview(B), memoryview(X), p, top, K, (p + 1) >> 1)
+        out["products"].append({"prime": key, "la": la, "lb": lb, "tally": [m, a]})
+    with open(os.path.join(HERE, "tallies.json"), "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(f"wrote tallies.json in {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
-    main()
+    if "--tallies" in sys.argv:
+        tallies()
+    else:
+        main()
+        tallies()

@@ -256,3 +256,26 @@ def test_shared_cta_small_tiles_against_oracle(golden, key):
         for v in range(cnt):
             assert np.array_equal(got[v], O.multiply(a[v * la:(v + 1) * la], b[v * lb:(v + 1) * lb],
                                                      cfg.p, cfg.omegaK, cfg.K)), (la, lb, v)
+
+
+def test_host_api_returns_reference_tallies(golden):
+    """_kernels-shaped calls return the reference walk's (mults, adds)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tallies.json")) as f:
+        tallies = json.load(f)
+    k = backend.kernels()
+    for case in tallies["transforms"][::7]:
+        p, top, K = golden["primes"][case["prime"]]
+        if case["n"] > (1 << 20):
+            continue
+        x = array("Q", bytes(8 * case["n"]))
+        assert list(k.tft(x, 0, case["n"], p, top, K)) == case["tft"]
+        assert list(k.itft(x, 0, case["n"], p, top, K, (p + 1) // 2)) == case["itft"]
+    for case in tallies["products"]:
+        p, top, K = golden["primes"][case["prime"]]
+        if case["la"] + case["lb"] > 200000:
+            continue
+        a, b = array("Q", bytes(8 * case["la"])), array("Q", bytes(8 * case["lb"]))
+        x = array("Q", bytes(8 * (case["la"] + case["lb"] - 1)))
+        assert list(k.multiply(a, b, x, p, top, K, (p + 1) // 2)) == case["tally"]

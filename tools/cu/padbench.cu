@@ -24,8 +24,39 @@ struct TwBcast {  // every thread reads the same twiddles (broadcast)
     TFT_DEV void get_many(int s, uint32_t, Tw<uint32_t>* out) const { ldg_tw_run<uint32_t, N>(Z + 32 * s, out); }
 };
 
-template <int P, int KK, int SLO, class TP>
-__device__ __forceinline__ void round_p(const F30& f, uint32_t* S, const TP& tp) {
+// single-word Montgomery twiddles: the table holds w R mod p (4 B); the
+// companion w R p^-1 mod 2^32 is one IMAD; b w = hi(b wR) - hi((b wRp) p) + p
+struct F30M : F30 {
+    TFT_DEV W mulw(W b, Tw<W> t) const { return __umulhi(b, t.w) - __umulhi(b * t.wp, p) + p; }
+    TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
+        W a = red2(x);
+        W b = mulw(y, t);
+        x = a + b;
+        y = a - b + p2;
+    }
+};
+struct TwWord {
+    const uint32_t* Zm;
+    uint32_t pinv;
+    TFT_DEV Tw<uint32_t> get(int, uint32_t J) const { const uint32_t w = __ldg(Zm + J); return Tw<uint32_t>{w, w * pinv}; }
+    template <int N>
+    TFT_DEV void get_many(int, uint32_t J0, Tw<uint32_t>* out) const {
+        if constexpr (N >= 4) {
+#pragma unroll
+            for (int q = 0; q < N; q += 4) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(Zm + J0 + q));
+                out[q] = Tw<uint32_t>{v.x, v.x * pinv}; out[q + 1] = Tw<uint32_t>{v.y, v.y * pinv};
+                out[q + 2] = Tw<uint32_t>{v.z, v.z * pinv}; out[q + 3] = Tw<uint32_t>{v.w, v.w * pinv};
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < N; ++q) out[q] = get(0, J0 + q);
+        }
+    }
+};
+
+template <int P, int KK, int SLO, class TP, class FF = F30>
+__device__ __forceinline__ void round_p(const FF& f, uint32_t* S, const TP& tp) {
     constexpr uint32_t NU = 1u << (14 - KK);
     constexpr uint32_t STEP = SLO >= 5 ? (1u << SLO) + (P << (SLO - 5)) : 1u;
     for (uint32_t g = threadIdx.x; g < NU; g += blockDim.x) {
@@ -43,7 +74,7 @@ __device__ __forceinline__ void round_p(const F30& f, uint32_t* S, const TP& tp)
 #pragma unroll
             for (int i = 0; i < (1 << KK); ++i) v[i] = pb[i * STEP];
         }
-        reg_fwd<F30, KK, KK - 1>(f, v, base, SLO, tp);
+        reg_fwd<FF, KK, KK - 1>(f, v, base, SLO, tp);
         if constexpr (SLO == 0 && KK == 5 && P == 4) {
             uint4* pv = reinterpret_cast<uint4*>(pb);
 #pragma unroll
@@ -56,7 +87,8 @@ __device__ __forceinline__ void round_p(const F30& f, uint32_t* S, const TP& tp)
 }
 
 template <int P, int SMALL>
-__global__ void __launch_bounds__(256, 3) kround(F30 f, const Tw<uint32_t>* Z, uint32_t* out, int reps) {
+__global__ void __launch_bounds__(256, 3) kround(F30 f, const Tw<uint32_t>* Z, uint32_t* out, int reps,
+                                                 const uint32_t* Zm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* S = reinterpret_cast<uint32_t*>(smem_raw);
     for (uint32_t i = threadIdx.x; i < 16384; i += blockDim.x) S[i + (i >> 5) * P] = i * 2654435761u % f.p;
@@ -67,7 +99,11 @@ __global__ void __launch_bounds__(256, 3) kround(F30 f, const Tw<uint32_t>* Z, u
         __syncthreads();
         round_p<P, 4, 5>(f, S, tp);
         __syncthreads();
-        if constexpr (SMALL == 2) round_p<P, 5, 0>(f, S, TwBcast{Z});
+        if constexpr (SMALL == 3) {
+            F30M fm;
+            static_cast<F30&>(fm) = f;
+            round_p<P, 5, 0, TwWord, F30M>(fm, S, TwWord{Zm, f.pinv});
+        } else if constexpr (SMALL == 2) round_p<P, 5, 0>(f, S, TwBcast{Z});
         else if constexpr (SMALL == 1) round_p<P, 5, 0>(f, S, TwSmall{Z});
         else round_p<P, 5, 0>(f, S, tp);
         __syncthreads();
@@ -76,14 +112,15 @@ __global__ void __launch_bounds__(256, 3) kround(F30 f, const Tw<uint32_t>* Z, u
 }
 
 template <int P, int SMALL>
-void run(F30 f, Tw<uint32_t>* Z, uint32_t* out) {
-    size_t smem = (16384 + 512 * P + P) * 4;
+void run(F30 f, Tw<uint32_t>* Z, uint32_t* out, size_t smem_force = 0, const uint32_t* Zm = nullptr) {
+    size_t smem = smem_force ? smem_force : (16384 + 512 * P + P) * 4;
+    printf("smem %zu: ", smem);
     cudaFuncSetAttribute(kround<P, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     int reps = 40, grid = 148 * 3 * 4;
     for (int k = 0; k < 3; ++k) {
         cudaEventRecord(a);
-        kround<P, SMALL><<<grid, 256, smem>>>(f, Z, out, reps);
+        kround<P, SMALL><<<grid, 256, smem>>>(f, Z, out, reps, Zm);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         double bf = (double)grid * reps * 14 * 8192;
@@ -105,4 +142,8 @@ int main() {
     run<1, 0>(f, Z, out);
     run<1, 1>(f, Z, out);
     run<1, 2>(f, Z, out);
+    std::vector<uint32_t> hm(1 << 16);
+    for (size_t j = 0; j < hm.size(); ++j) hm[j] = (uint32_t)(((unsigned __int128)h[j].w << 32) % p);
+    uint32_t* Zm; cudaMalloc(&Zm, hm.size() * 4); cudaMemcpy(Zm, hm.data(), hm.size() * 4, cudaMemcpyHostToDevice);
+    run<1, 3>(f, Z, out, 0, Zm);
 }
