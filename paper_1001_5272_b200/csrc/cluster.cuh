@@ -25,6 +25,12 @@
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
+#include <type_traits>
+
+// CTAs per SM the 256-thread tile kernels are compiled for: 3 (80 registers)
+// for u32 words; u64 words need twice the registers per 32-word unit, so 2
+template <class F>
+constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : 3; }
 
 namespace cg = cooperative_groups;
 
@@ -269,7 +275,7 @@ TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint
 }
 
 // ------------------------------------------------------------ kernels
-template <class F, int CL, int MINB = 3, int NT = 256>
+template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
 __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -416,7 +422,7 @@ TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg
     }
 }
 
-template <class F, int CL, int MINB = 3, int NT = 256>
+template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
 __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
 // Chunks are 2^CL contiguous words = sub-block k of the network at level CL;
 // twiddles come from TwBig (block k).  grid: (max chunks, vectors).
 template <class F, int CL>
-__global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_chunk_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -513,7 +519,7 @@ __global__ void __launch_bounds__(256, 3) k_chunk_fwd(LaunchArgs<F> a) {
 // needs nothing from the columns) so the serial step 3 only runs the two
 // O(2^CL) sweeps.  grid: (max chunks, vectors)
 template <class F, int CL>
-__global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_chunk_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(256, 3) k_chunk_inv(LaunchArgs<F> a) {
 // step 3: the partial last chunk: its h slots already hold the phase-1
 // values (k_chunk_inv); the C-h stashed inputs complete it.  grid: (1, vectors)
 template <class F, int CL>
-__global__ void __launch_bounds__(256, 3) k_last_inv(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_last_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -722,7 +728,7 @@ TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, cons
 }
 
 template <class F, int CL, int GAM>
-__global__ void __launch_bounds__(256, 3) k_clg_fwd(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);

@@ -62,10 +62,9 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     if (pl.kind == kCluster) {
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
-        static const int minb = getenv("TFTB_CL_MINB") ? atoi(getenv("TFTB_CL_MINB")) : 3;  // tuning knob
-        const int nt = minb == 4 ? 512 : 256;  // 4 -> 512-thread CTAs, 2 per SM
-        auto kf = minb == 2 ? k_cl_fwd<F, CL, 2> : (minb == 4 ? k_cl_fwd<F, CL, 2, 512> : k_cl_fwd<F, CL, 3>);
-        auto ki = minb == 2 ? k_cl_inv<F, CL, 2> : (minb == 4 ? k_cl_inv<F, CL, 2, 512> : k_cl_inv<F, CL, 3>);
+        const int nt = kNT;
+        auto kf = k_cl_fwd<F, CL>;
+        auto ki = k_cl_inv<F, CL>;
         if (set_smem(kf, smem) || set_smem(ki, smem)) return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;

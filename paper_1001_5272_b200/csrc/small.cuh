@@ -23,12 +23,8 @@ struct TileShape {
     static constexpr size_t smem(size_t wbytes) { return (size_t)VPB * WORDS * wbytes; }
 };
 
-// u64 words need twice the registers per unit: 2 CTAs per SM for them
-template <class F>
-constexpr int tile_minb() { return sizeof(typename F::W) == 8 ? 2 : 3; }
-
 template <class F, int T>
-__global__ void __launch_bounds__(256, tile_minb<F>()) k_tile_fwd(LaunchArgs<F> a, int64_t vend) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_fwd(LaunchArgs<F> a, int64_t vend) {
     using W = typename F::W;
     using SH = TileShape<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -51,7 +47,7 @@ __global__ void __launch_bounds__(256, tile_minb<F>()) k_tile_fwd(LaunchArgs<F> 
 }
 
 template <class F, int T>
-__global__ void __launch_bounds__(256, tile_minb<F>()) k_tile_inv(LaunchArgs<F> a, int64_t vend) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_inv(LaunchArgs<F> a, int64_t vend) {
     using W = typename F::W;
     using SH = TileShape<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
