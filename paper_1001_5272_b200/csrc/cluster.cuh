@@ -63,14 +63,88 @@ TFT_DEV void ldg_tw_run(const Tw<W>* p, Tw<W>* out) {
     }
 }
 
+// N consecutive single-word (Montgomery) twiddles -> Tw pairs {wR, wR p^-1},
+// 16-byte loads where N allows (runs are N-aligned)
+template <int N>
+TFT_DEV void ldg_word_run(const uint32_t* p, uint32_t pinv, Tw<uint32_t>* out) {
+    if constexpr (N >= 4) {
+#pragma unroll
+        for (int q = 0; q < N; q += 4) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(p + q));
+            out[q] = Tw<uint32_t>{t.x, t.x * pinv};
+            out[q + 1] = Tw<uint32_t>{t.y, t.y * pinv};
+            out[q + 2] = Tw<uint32_t>{t.z, t.z * pinv};
+            out[q + 3] = Tw<uint32_t>{t.w, t.w * pinv};
+        }
+    } else if constexpr (N == 2) {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        out[0] = Tw<uint32_t>{t.x, t.x * pinv};
+        out[1] = Tw<uint32_t>{t.y, t.y * pinv};
+    } else {
+        const uint32_t w = __ldg(p);
+        out[0] = Tw<uint32_t>{w, w * pinv};
+    }
+}
+
+// TwDirect over the single-word table (F30M twiddles)
+struct TwDirectM {
+    const uint32_t* ZM;
+    uint32_t blk;
+    int T;
+    uint32_t pinv;
+    TFT_DEV Tw<uint32_t> get(int s, uint32_t J) const {
+        const uint32_t w = __ldg(ZM + ((blk << (T - s - 1)) + J));
+        return Tw<uint32_t>{w, w * pinv};
+    }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<uint32_t>* out) const {
+        ldg_word_run<N>(ZM + ((blk << (T - s - 1)) + J0), pinv, out);
+    }
+};
+
+// TwBig over the single-word tables: above 2^zb the product of the two
+// Montgomery words is one REDC (mont(hR, lR) = hlR), its companion one IMAD
+struct TwBigM {
+    const uint32_t* ZM;
+    const uint32_t* ZhM;
+    uint64_t blk;
+    int T, zb;
+    F30 f;
+    TFT_DEV Tw<uint32_t> get(int s, uint32_t J) const {
+        Tw<uint32_t> t[1];
+        get_many<1>(s, J, t);
+        return t[0];
+    }
+    template <int N>
+    TFT_DEV void get_many(int s, uint32_t J0, Tw<uint32_t>* out) const {
+        const uint64_t idx = (blk << (T - s - 1)) + J0;
+        const uint64_t m = (1ull << zb) - 1;
+        ldg_word_run<N>(ZM + (idx & m), f.pinv, out);
+        if (idx > m) {
+            const uint32_t hi = __ldg(ZhM + (idx >> zb));
+#pragma unroll
+            for (int q = 0; q < N; ++q) {
+                const uint32_t w = f.red1(f.mont(hi, out[q].w));
+                out[q] = Tw<uint32_t>{w, w * f.pinv};
+            }
+        }
+    }
+};
+
 // Direct twiddles for a tile that is block `blk` at level T:
 // theta(s, J) = omega_{2 (blk 2^(T-s-1) + J)} from the 2^zb-entry table.
+// ZM: the same table as single Montgomery words; the bottom (SLO = 0) rounds
+// of a Shoup field use it (their twiddles are per thread), so providers for
+// F30 that reach the rounds must carry it.
 template <class F>
 struct TwDirect {
+    static constexpr bool kMont = true;
     const Tw<typename F::W>* Z;
     uint32_t blk;
     int T;
     F f;
+    const typename F::W* ZM = nullptr;
+    TFT_DEV TwDirectM mont() const { return TwDirectM{(const uint32_t*)ZM, blk, T, (uint32_t)f.pinv}; }
     TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const { return ldg_tw(Z + ((blk << (T - s - 1)) + J)); }
     template <int N>
     TFT_DEV void get_many(int s, uint32_t J0, Tw<typename F::W>* out) const {
@@ -86,11 +160,19 @@ struct TwDirect {
 // boundary.
 template <class F>
 struct TwBig {
+    static constexpr bool kMont = true;
     const Tw<typename F::W>* Z;
     const Tw<typename F::W>* Zh;
     uint64_t blk;
     int T, zb;
     F f;
+    const typename F::W* ZM = nullptr;  // single-word tables (see TwDirect)
+    const typename F::W* ZhM = nullptr;
+    TFT_DEV TwBigM mont() const {
+        F30 g;
+        if constexpr (std::is_same<F, F30>::value) g = f;
+        return TwBigM{(const uint32_t*)ZM, (const uint32_t*)ZhM, blk, T, zb, g};
+    }
     TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
         const uint64_t idx = (blk << (T - s - 1)) + J;
         const uint64_t m = (1ull << zb) - 1;
@@ -129,7 +211,7 @@ TFT_DEV constexpr uint32_t unit_off(int i) {
 // Forward round.  With PRUNE, units whose every output row is >= lim are
 // skipped (only rows < lim are needed after the remaining stages).
 template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
-TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
+TFT_DEV void fwd_round_units(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t lim = PRUNE ? ((need + (1u << SLO) - 1) >> SLO) << SLO : 0;
@@ -152,8 +234,8 @@ TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t n
 // blocks of [0, h) run, each block scaled at its last stage (tile.cuh
 // reg_inv); SCALE=false leaves an unmasked tile scaled by 2^TL.
 template <class F, int TL, int KK, int SLO, int WLOG, bool MASK, bool SCALE, class TP>
-TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
-                          uint32_t h, Lanes ln) {
+TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
+                             uint32_t h, Lanes ln) {
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
     const uint32_t h_lo = MASK ? (uint32_t)(((uint64_t)h >> (SLO + 1)) << (SLO + 1)) : 0;
@@ -185,6 +267,34 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
     }
+}
+
+// In the bottom round (SLO = 0) every thread needs its own 2^KK - 1
+// twiddles -- about one per tile word, more bytes than the tile itself in
+// 8-byte Shoup pairs.  For a Shoup field whose provider carries the
+// single-word tables that round multiplies by Montgomery words instead
+// (F30M: half the twiddle bytes for one more IMAD.HI per butterfly).
+template <class F, class TP>
+__host__ __device__ constexpr bool bottom_mont() {
+    if constexpr (std::is_same<F, F30>::value) return TP::kMont;
+    else return false;
+}
+
+template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
+TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
+    if constexpr (SLO == 0 && WLOG == 0 && bottom_mont<F, TP>())
+        fwd_round_units<F30M, TL, KK, SLO, WLOG, PRUNE>(F30M(f), S, tp.mont(), need, ln);
+    else
+        fwd_round_units<F, TL, KK, SLO, WLOG, PRUNE>(f, S, tp, need, ln);
+}
+
+template <class F, int TL, int KK, int SLO, int WLOG, bool MASK, bool SCALE, class TP>
+TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
+                          uint32_t h, Lanes ln) {
+    if constexpr (SLO == 0 && WLOG == 0 && bottom_mont<F, TP>())
+        inv_round_units<F30M, TL, KK, SLO, WLOG, MASK, SCALE>(F30M(f), S, tp.mont(), ipow2, h, ln);
+    else
+        inv_round_units<F, TL, KK, SLO, WLOG, MASK, SCALE>(f, S, tp, ipow2, h, ln);
 }
 
 // stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),
@@ -308,7 +418,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
     TFTB_STAMP(a, 4);
 
     // only this chunk's rows below n are outputs: prune the rest
-    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f}, (uint32_t)min((int64_t)C, n - cbase));
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f, a.R.ZfM}, (uint32_t)min((int64_t)C, n - cbase));
     TFTB_STAMP(a, 5);
 
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
@@ -446,7 +556,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     TFTB_STAMP(a, 1);
     // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
     // known outputs [0, h), never the tail the columns will fill) alongside
-    const TwDirect<F> tpi{a.R.Zi, g, CL, f};
+    const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
     // complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
     if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
@@ -509,7 +619,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_chunk_fwd(LaunchArgs<F>
     const int64_t avail = n - cbase;
     tile_load<W>(S, x, avail, C, [&](uint32_t i, W w) { return (int64_t)i < avail ? w : st[i]; });
     __syncthreads();
-    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwBig<F>{a.R.Zf, a.R.Zfh, k, CL, a.R.zb, f},
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwBig<F>{a.R.Zf, a.R.Zfh, k, CL, a.R.zb, f, a.R.ZfM, a.R.ZfhM},
                                       (uint32_t)min((int64_t)C, avail));
     tile_store<W>(x, S, (uint32_t)min((int64_t)C, avail), [&](W w) { return f.canon(w); });
 }
@@ -540,7 +650,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_chunk_inv(LaunchArgs<F>
     else
         tile_load<W>(S, x, len, C, [](uint32_t, W w) { return w; });
     __syncthreads();
-    const TwBig<F> tpi{a.R.Zi, a.R.Zih, k, CL, a.R.zb, f};
+    const TwBig<F> tpi{a.R.Zi, a.R.Zih, k, CL, a.R.zb, f, a.R.ZiM, a.R.ZihM};
     if (k < K) inv_rounds_ct<F, CL, CL, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
     tile_store<W>(x, S, len, [&](W w) { return f.canon(w); });
@@ -804,7 +914,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
     TFTB_STAMP(a, 1);
     __syncthreads();
     TFTB_STAMP(a, 2);
-    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f}, (uint32_t)min((int64_t)C, n - cbase));
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f, a.R.ZfM}, (uint32_t)min((int64_t)C, n - cbase));
     TFTB_STAMP(a, 5);
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });

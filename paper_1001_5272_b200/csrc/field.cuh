@@ -51,6 +51,8 @@ struct F30 {
         return Tw<W>{w, (0u - r) * pinv};
     }
     TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return red1(mulw(a.w, b)); }
+    // b * (constant scale factor, a Shoup pair): [0, 2p)
+    TFT_DEV W scale(W b, Tw<W> t) const { return mulw(b, t); }
     // REDC a*b/2^32 for a*b < p 2^32: [0, 2p)
     TFT_DEV W mont(W a, W b) const {
         const uint64_t ab = (uint64_t)a * b;
@@ -87,6 +89,30 @@ struct F30 {
     TFT_DEV W cmulw(W b, Tw<W> t) const { return red1(mulw(b, t)); }
 };
 
+// F30 with single-word twiddles: the twiddle is w R mod p (R = 2^32) and its
+// companion w R p^-1 mod R is one IMAD from it, so a twiddle costs 4 bytes of
+// table instead of 8.  b w = hi(b wR) - hi((b wRp) p) + p in (0, 2p) for any
+// 32-bit b: two IMAD.HI + one IMAD, against Shoup's one IMAD.HI + two IMAD.
+// Used where twiddles are per-thread (the bottom 5 stages), so table bytes,
+// not the integer pipe, are the limit.  Constant scale factors stay Shoup.
+struct F30M : F30 {
+    TFT_DEV explicit F30M(const F30& f) : F30(f) {}
+    TFT_DEV W mulw(W b, Tw<W> t) const { return __umulhi(b, t.w) - __umulhi(b * t.wp, p) + p; }
+    TFT_DEV W scale(W b, Tw<W> t) const { return F30::mulw(b, t); }
+    TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
+        W a = red2(x);
+        W b = mulw(y, t);
+        x = a + b;
+        y = a - b + p2;
+    }
+    TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
+        W s = red2(x + y);
+        W d = x - y + p2;
+        x = s;
+        y = mulw(d, t);
+    }
+};
+
 struct F32 {
     using W = uint32_t;
     static constexpr bool kLazy = false;
@@ -112,6 +138,7 @@ struct F32 {
     }
     TFT_DEV Tw<W> tw(W wM) const { return Tw<W>{wM, wM * pinv}; }
     TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return mont(a.w, b.w); }
+    TFT_DEV W scale(W b, Tw<W> t) const { return mulw(b, t); }
     TFT_DEV W cadd(W a, W b) const {
         W s = a + b;
         return (s < a || s >= p) ? s - p : s;
@@ -161,6 +188,7 @@ struct F62 {
     }
     TFT_DEV Tw<W> tw(W wM) const { return Tw<W>{wM, wM * pinv}; }
     TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return red1(mont(a.w, b.w)); }
+    TFT_DEV W scale(W b, Tw<W> t) const { return mulw(b, t); }
     TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
         W a = red2(x);
         W b = mulw(y, t);

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_fwd(LaunchArgs<F> 
         tile_load<W>(S, a.in + a.ind.o(v), a.ind.n(v), 1u << T, [](uint32_t, W w) { return w; }, ln);
     }
     __syncthreads();
-    if constexpr (T > 0) fwd_rounds_ct<F, T, T, 0, true>(f, S, TwDirect<F>{a.R.Zf, 0, T, f}, (uint32_t)n, ln);
+    if constexpr (T > 0) fwd_rounds_ct<F, T, T, 0, true>(f, S, TwDirect<F>{a.R.Zf, 0, T, f, a.R.ZfM}, (uint32_t)n, ln);
     if (live) tile_store<W>(x, S, (uint32_t)n, [&](W w) { return f.canon(w); }, ln);
 }
 
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_inv(LaunchArgs<F> 
     __syncthreads();
     // phase 1 (n = 2^T: the plain scaled inverse), then phases 2/3
     const uint32_t h = (uint32_t)n;
-    const TwDirect<F> tpi{a.R.Zi, 0, T, f};
+    const TwDirect<F> tpi{a.R.Zi, 0, T, f, a.R.ZiM};
     if constexpr (T > 0) {  // (a 1-point transform is the identity)
         inv_rounds_ct<F, T, T, true>(f, S, tpi, a.R.ipow2, h, ln);
         itft_phases23(f, SmemTile<W>{S, T, 0}, h, TwDirect<F>{a.R.Zf, 0, T, f}, tpi, a.R, ln, SH::VPB > 1);

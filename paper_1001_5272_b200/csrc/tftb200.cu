@@ -141,6 +141,16 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
             }
         for (size_t i = 0; i < raw.size(); i += 2) host.push_back(Tw<W>{raw[i], raw[i + 1]});
     }
+    // single-word twiddle tables (w R mod p) for the bottom rounds of a
+    // Shoup field (cluster.cuh TwDirectM/TwBigM): Zf, Zi, Zfh, Zih
+    const size_t mword_off = host.size();
+    if (tb.shoup) {
+        std::vector<W> mw;
+        for (auto* z : {&zf, &zi, &zfh, &zih})
+            for (auto v : *z) mw.push_back((W)tb.to_m(v));
+        if (mw.size() & 1) mw.push_back(0);
+        for (size_t i = 0; i < mw.size(); i += 2) host.push_back(Tw<W>{mw[i], mw[i + 1]});
+    }
     size_t tw_bytes = host.size() * sizeof(Tw<W>);
     CK(cudaMalloc(&rh->dmem, tw_bytes));
     CK(cudaMemcpy(rh->dmem, host.data(), tw_bytes, cudaMemcpyHostToDevice));
@@ -154,6 +164,15 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     out->vinvS = out->vinv + 8 * 72;
     out->vinvT = out->vinv + 16 * 72;
     out->vinvM = reinterpret_cast<const W*>(out->vinv + 24 * 72);
+    if (tb.shoup) {
+        const W* mw = reinterpret_cast<const W*>(d + mword_off);
+        out->ZfM = mw;
+        out->ZiM = mw + nz;
+        out->ZfhM = mw + 2 * nz;
+        out->ZihM = mw + 2 * nz + nh;
+    } else {
+        out->ZfM = out->ZiM = out->ZfhM = out->ZihM = nullptr;
+    }
     uint64_t R1 = tb.to_m(1);
     out->r2w = (W)tb.to_m(R1);  // R^2 mod p
     out->inv2 = tb.tw(inv2);

@@ -50,6 +50,10 @@ struct RingDev {
     const Tw<W>* vinvS; // same with every column times 2^-CL
     const Tw<W>* vinvT; // same with all but the last column times 2^-CL
     const W* vinvM;     // vinv, vinvS, vinvT as raw Montgomery words (3 x 8 x 72)
+    const W* ZfM;       // Zf, Zi, Zfh, Zih as single Montgomery words w R mod p
+    const W* ZiM;       // (Shoup fields only, else null): the bottom rounds'
+    const W* ZfhM;      // per-thread twiddles at half the bytes
+    const W* ZihM;
     Tw<W> inv2;         // 1/2
     W r2w;              // R^2 mod p as a raw word: mont(mont(a, b), r2w) = a b
     W oneW;             // 1 as a field word (1, or R mod p for Montgomery fields)
@@ -89,6 +93,7 @@ TFT_DEV typename F::W pow_w(const F& f, typename F::W base, typename F::W one, u
 // ---------------------------------------------------------------- twiddles
 template <class F>
 struct TwPrefix {  // untwisted tile: theta(s, J) = Z[J]
+    static constexpr bool kMont = false;
     const Tw<typename F::W>* Z;
     TFT_DEV Tw<typename F::W> get(int, uint32_t J) const { return Z[J]; }
     template <int N>
@@ -146,8 +151,8 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
             if (MASK && pos >= hs) continue;
             f.inv(v[i], v[i | (1 << ST)], t);
             if (MASK ? pos >= hs1 : scale_all) {
-                v[i] = f.mulw(v[i], sc);
-                v[i | (1 << ST)] = f.mulw(v[i | (1 << ST)], sc);
+                v[i] = f.scale(v[i], sc);
+                v[i | (1 << ST)] = f.scale(v[i | (1 << ST)], sc);
             }
         }
     }
