@@ -104,12 +104,13 @@ struct TwDirectM {
 
 // TwBig over the single-word tables: above 2^zb the product of the two
 // Montgomery words is one REDC (mont(hR, lR) = hlR), its companion one IMAD
+template <class FM>
 struct TwBigM {
     const uint32_t* ZM;
     const uint32_t* ZhM;
     uint64_t blk;
     int T, zb;
-    F30 f;
+    FM f;
     TFT_DEV Tw<uint32_t> get(int s, uint32_t J) const {
         Tw<uint32_t> t[1];
         get_many<1>(s, J, t);
@@ -168,11 +169,7 @@ struct TwBig {
     F f;
     const typename F::W* ZM = nullptr;  // single-word tables (see TwDirect)
     const typename F::W* ZhM = nullptr;
-    TFT_DEV TwBigM mont() const {
-        F30 g;
-        if constexpr (std::is_same<F, F30>::value) g = f;
-        return TwBigM{(const uint32_t*)ZM, (const uint32_t*)ZhM, blk, T, zb, g};
-    }
+    TFT_DEV TwBigM<F> mont() const { return TwBigM<F>{(const uint32_t*)ZM, (const uint32_t*)ZhM, blk, T, zb, f}; }
     TFT_DEV Tw<typename F::W> get(int s, uint32_t J) const {
         const uint64_t idx = (blk << (T - s - 1)) + J;
         const uint64_t m = (1ull << zb) - 1;
@@ -271,30 +268,40 @@ TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const T
 
 // In the bottom round (SLO = 0) every thread needs its own 2^KK - 1
 // twiddles -- about one per tile word, more bytes than the tile itself in
-// 8-byte Shoup pairs.  For a Shoup field whose provider carries the
-// single-word tables that round multiplies by Montgomery words instead
-// (F30M: half the twiddle bytes for one more IMAD.HI per butterfly).
+// 8-byte pairs.  For u32 words that round reads the single-word tables
+// instead: Montgomery words whose companion is one IMAD.  For p < 2^32 the
+// product is unchanged (F32 is Montgomery already); for p < 2^30 it becomes
+// F30M's Montgomery product (one more IMAD.HI than Shoup per butterfly).
 template <class F, class TP>
-__host__ __device__ constexpr bool bottom_mont() {
-    if constexpr (std::is_same<F, F30>::value) return TP::kMont;
+__host__ __device__ constexpr bool bottom_words() {
+    if constexpr (std::is_same<F, F30>::value || std::is_same<F, F32>::value) return TP::kMont;
     else return false;
+}
+template <class F>
+TFT_DEV auto bottom_field(const F& f) {
+    if constexpr (std::is_same<F, F30>::value) return F30M(f);
+    else return f;
 }
 
 template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
 TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
-    if constexpr (SLO == 0 && WLOG == 0 && bottom_mont<F, TP>())
-        fwd_round_units<F30M, TL, KK, SLO, WLOG, PRUNE>(F30M(f), S, tp.mont(), need, ln);
-    else
+    if constexpr (SLO == 0 && WLOG == 0 && bottom_words<F, TP>()) {
+        const auto fb = bottom_field(f);
+        fwd_round_units<decltype(fb), TL, KK, SLO, WLOG, PRUNE>(fb, S, tp.mont(), need, ln);
+    } else {
         fwd_round_units<F, TL, KK, SLO, WLOG, PRUNE>(f, S, tp, need, ln);
+    }
 }
 
 template <class F, int TL, int KK, int SLO, int WLOG, bool MASK, bool SCALE, class TP>
 TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<typename F::W>* ipow2,
                           uint32_t h, Lanes ln) {
-    if constexpr (SLO == 0 && WLOG == 0 && bottom_mont<F, TP>())
-        inv_round_units<F30M, TL, KK, SLO, WLOG, MASK, SCALE>(F30M(f), S, tp.mont(), ipow2, h, ln);
-    else
+    if constexpr (SLO == 0 && WLOG == 0 && bottom_words<F, TP>()) {
+        const auto fb = bottom_field(f);
+        inv_round_units<decltype(fb), TL, KK, SLO, WLOG, MASK, SCALE>(fb, S, tp.mont(), ipow2, h, ln);
+    } else {
         inv_round_units<F, TL, KK, SLO, WLOG, MASK, SCALE>(f, S, tp, ipow2, h, ln);
+    }
 }
 
 // stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),

@@ -141,10 +141,11 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
             }
         for (size_t i = 0; i < raw.size(); i += 2) host.push_back(Tw<W>{raw[i], raw[i + 1]});
     }
-    // single-word twiddle tables (w R mod p) for the bottom rounds of a
-    // Shoup field (cluster.cuh TwDirectM/TwBigM): Zf, Zi, Zfh, Zih
+    // single-word twiddle tables (w R mod p) for the bottom rounds of u32
+    // rings (cluster.cuh TwDirectM/TwBigM): Zf, Zi, Zfh, Zih
     const size_t mword_off = host.size();
-    if (tb.shoup) {
+    constexpr bool words = sizeof(W) == 4;
+    if (words) {
         std::vector<W> mw;
         for (auto* z : {&zf, &zi, &zfh, &zih})
             for (auto v : *z) mw.push_back((W)tb.to_m(v));
@@ -164,7 +165,7 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     out->vinvS = out->vinv + 8 * 72;
     out->vinvT = out->vinv + 16 * 72;
     out->vinvM = reinterpret_cast<const W*>(out->vinv + 24 * 72);
-    if (tb.shoup) {
+    if (words) {
         const W* mw = reinterpret_cast<const W*>(d + mword_off);
         out->ZfM = mw;
         out->ZiM = mw + nz;
