@@ -1,5 +1,6 @@
 // Batch planning and launches (instantiated once per field type).
 #pragma once
+#include "p2r.cuh"
 #include "small.cuh"
 #include "host.h"
 
@@ -39,6 +40,70 @@ int run_tiles(LaunchArgs<F> a, int T, int64_t count, bool inverse, cudaStream_t 
     }
     return fail("tile size class out of range");
 }
+
+static_assert(kP2RMax == kP2RMaxDev, "p2r bound mismatch");
+
+// omega_s (modring.py:223-234) on the host
+inline uint64_t omega_host(const RingHost* rh, uint64_t s) {
+    if (!s) return 1;
+    const int k = 64 - __builtin_clzll(s);
+    uint64_t rev = 0;
+    for (int i = 0; i < k; ++i) rev |= ((s >> i) & 1) << (k - 1 - i);
+    return powmod(powmod(rh->top, 1ull << (rh->K - k), rh->p), rev, rh->p);
+}
+
+// a field twiddle for w (canonical residue): Shoup pair for F30, Montgomery
+// pair otherwise (the device forms, field.cuh)
+template <class F>
+Tw<typename F::W> host_tw(uint64_t w, uint64_t p) {
+    using W = typename F::W;
+    constexpr int bits = 8 * sizeof(W);
+    if constexpr (std::is_same<F, F30>::value) {
+        return Tw<W>{(W)w, (W)(((u128)w << 32) / p)};
+    } else {
+        const W wm = (W)(((u128)w << bits) % p);
+        return Tw<W>{wm, (W)(wm * inv_word<W>((W)p))};
+    }
+}
+
+// the powers k_p2r reads, per s < r: rho_s, rho_s^(1024 nb), rho_s^(4t)
+// (t < 256), rho_s^(1024 b) (b < nb) -- built once per (ring, k, r, nb)
+template <class F>
+const Tw<typename F::W>* p2r_tables(const RingHost* rh, int k, int r, int nb) {
+    using W = typename F::W;
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int, int, int>, void*> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    void*& d = cache[{(const void*)rh, k, r, nb, dev}];
+    if (!d) {
+        const uint64_t p = rh->p;
+        std::vector<Tw<W>> h;
+        for (int s = 0; s < r; ++s) {
+            const uint64_t rho = omega_host(rh, (1ull << k) + s);
+            h.push_back(host_tw<F>(rho, p));
+            h.push_back(host_tw<F>(powmod(rho, 1024ull * nb, p), p));
+            const uint64_t r4 = powmod(rho, 4, p), r1024 = powmod(rho, 1024, p);
+            uint64_t w = 1;
+            for (int t = 0; t < 256; ++t, w = mulmod(w, r4, p)) h.push_back(host_tw<F>(w, p));
+            w = 1;
+            for (int b = 0; b < nb; ++b, w = mulmod(w, r1024, p)) h.push_back(host_tw<F>(w, p));
+        }
+        if (cudaMalloc(&d, h.size() * sizeof(Tw<W>)) != cudaSuccess ||
+            cudaMemcpy(d, h.data(), h.size() * sizeof(Tw<W>), cudaMemcpyHostToDevice) != cudaSuccess) {
+            d = nullptr;
+            fail("p2r: table upload failed");
+            return nullptr;
+        }
+    }
+    return (const Tw<W>*)d;
+}
+
+// n = 2^k + r: fold + r dot products + the 2^k transform (p2r.cuh)
+template <class F>
+int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, VecDesc<typename F::W> xd,
+            bool inverse, cudaStream_t st, typename F::W* stash_buf);
 
 // One group of vectors that share a plan.
 template <class F>
@@ -100,6 +165,13 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         return 0;
     }
     if (pl.kind == kSmall) return run_tiles<F>(a, pl.l, count, inverse, st);
+    if (pl.kind == kP2R) {
+        if (in && in != x) {  // the fold rewrites the input: transforms in place only
+            if (make_plan<F>(maxn, &pl, false)) return -1;
+        } else {
+            return run_p2r<F>(rh, a, pl.l - 1, pl.G, count, xd, inverse, st, stash_buf);
+        }
+    }
     const uint32_t C = 1u << pl.l1;
     const int64_t maxchunks = (maxn + C - 1) / C;
     const int64_t vchunk = 65535;
@@ -153,6 +225,74 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
 // Build a reusable batch plan: vectors grouped by kernel plan, per-group
 // device offset/length arrays and the largest stash, all allocated once.
 template <class F>
+int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, VecDesc<typename F::W> xd,
+            bool inverse, cudaStream_t st, typename F::W* stash_buf) {
+    using W = typename F::W;
+    const int64_t H = 1ll << k;
+    VecDesc<W> pre_d = xd;  // the 2^k prefix of every vector
+    pre_d.len = nullptr;
+    pre_d.n0 = H;
+    // blocks per vector: ~8 per SM over the whole batch (full occupancy for a
+    // streaming pass; per-thread setup is a few table loads)
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (8 * 148 + count - 1) / count));
+    const Tw<W>* tab = p2r_tables<F>(rh, k, r, nb);
+    if (!tab) return -1;
+    const int64_t vchunk = 65535;
+    const int64_t cmax = std::min(count, vchunk);
+    Scratch part;
+    if (part.get((size_t)cmax * nb * kP2RMax * sizeof(W) + (size_t)cmax * sizeof(unsigned), st)) return -1;
+    unsigned* ticket = reinterpret_cast<unsigned*>((W*)part.p + (size_t)cmax * nb * kP2RMax);
+    CK(cudaMemsetAsync(ticket, 0, (size_t)cmax * sizeof(unsigned), st));
+    P2RConsts<F> c{};
+    auto launch = [&](bool inv) -> int {
+        for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
+            a.vbase = v0;
+            const unsigned nv = (unsigned)std::min(count - v0, vchunk);
+            if (inv) k_p2r<F, true><<<dim3(nb, nv), 256, 0, st>>>(a, k, r, H, (W*)part.p, ticket, tab, c);
+            else k_p2r<F, false><<<dim3(nb, nv), 256, 0, st>>>(a, k, r, H + r, (W*)part.p, ticket, tab, c);
+            g_launches++;
+            CK(cudaGetLastError());
+        }
+        return 0;
+    };
+    if (!inverse) {
+        if (launch(false)) return -1;
+        return run_group<F>(rh, a.x, nullptr, nullptr, count, pre_d, pre_d, H, false, st, stash_buf);
+    }
+    if (run_group<F>(rh, a.x, nullptr, a.pre, count, pre_d, pre_d, H, true, st, stash_buf)) return -1;
+    // V[s][t] = rho_s^t, rho_s = omega_{2^k + s}: its inverse on the host
+    {
+        const uint64_t p = rh->p;
+        uint64_t A[kP2RMax][2 * kP2RMax] = {};
+        for (int s2 = 0; s2 < r; ++s2) {
+            const uint64_t rho = omega_host(rh, (uint64_t)H + s2);
+            uint64_t pw = 1;
+            for (int t = 0; t < r; ++t) {
+                A[s2][t] = pw;
+                pw = mulmod(pw, rho, p);
+            }
+            A[s2][r + s2] = 1;
+        }
+        for (int col = 0; col < r; ++col) {
+            int piv = col;
+            while (piv < r && !A[piv][col]) ++piv;
+            if (piv == r) return fail("p2r: singular Vandermonde system");
+            for (int q = 0; q < 2 * r; ++q) std::swap(A[col][q], A[piv][q]);
+            const uint64_t inv = powmod(A[col][col], p - 2, p);
+            for (int q = 0; q < 2 * r; ++q) A[col][q] = mulmod(A[col][q], inv, p);
+            for (int row = 0; row < r; ++row) {
+                if (row == col || !A[row][col]) continue;
+                const uint64_t fct = A[row][col];
+                for (int q = 0; q < 2 * r; ++q) A[row][q] = (A[row][q] + p - mulmod(fct, A[col][q], p)) % p;
+            }
+        }
+        for (int t = 0; t < r; ++t)
+            for (int s2 = 0; s2 < r; ++s2) c.vinv[t][s2] = host_tw<F>(A[t][r + s2], p);
+    }
+    return launch(true);
+}
+
+template <class F>
 int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
                 const int64_t* h_len, PlanImpl* P) {
     using W = typename F::W;
@@ -180,8 +320,8 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
         }
         Plan pl;
         make_plan<F>(g.maxn, &pl);
-        if (pl.kind == kLarge)
-            stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << pl.l1);
+        if (pl.kind == kLarge || pl.kind == kP2R)  // (p2r: its 2^k prefix runs the two-pass plan)
+            stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << Limits<F>::CL);
         g.arr_off = words;
         words += 2 * g.count;
         P->host_arrays.insert(P->host_arrays.end(), off.begin(), off.end());

@@ -108,17 +108,24 @@ struct Limits {
     static constexpr int col_t = sizeof(typename F::W) == 4 ? 14 : 13;
 };
 
-enum PlanKind { kSmall = 0, kCluster = 1, kLarge = 2 };
+enum PlanKind { kSmall = 0, kCluster = 1, kLarge = 2, kP2R = 3 };
+
+// n = 2^k + r with r <= kP2RMax beyond the cluster range runs as the 2^k
+// transform plus r dot products (p2r.cuh) instead of a half-empty two-pass plan
+constexpr int kP2RMax = 4;
 
 struct Plan {
     PlanKind kind;
     int l, l0, l1, wlog, G;
     // small vectors group by tile size class, cluster ones by chunk count
-    int key() const { return kind == kSmall ? -100 + l : (kind == kCluster ? 1000 + G : l); }
+    // (p2r: n itself, as 2^(l-1) + G)
+    int key() const {
+        return kind == kSmall ? -100 + l : kind == kCluster ? 1000 + G : kind == kP2R ? 3000 + 8 * l + G : l;
+    }
 };
 
 template <class F>
-int make_plan(int64_t n, Plan* pl) {
+int make_plan(int64_t n, Plan* pl, bool p2r_ok = true) {
     const int l = ceil_lg(n);
     pl->l = l;
     pl->l0 = pl->l1 = pl->wlog = 0;
@@ -132,6 +139,12 @@ int make_plan(int64_t n, Plan* pl) {
     if (n <= (8ll << CL) && !no_cluster) {
         pl->kind = kCluster;
         pl->G = (int)((n + (1ll << CL) - 1) >> CL);
+        return 0;
+    }
+    static const bool no_p2r = getenv("TFTB_NO_P2R") != nullptr;  // A/B knob
+    if (p2r_ok && !no_p2r && l - 1 > CL + 3 && n - (1ll << (l - 1)) <= kP2RMax) {
+        pl->kind = kP2R;
+        pl->G = (int)(n - (1ll << (l - 1)));
         return 0;
     }
     pl->kind = kLarge;

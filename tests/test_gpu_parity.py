@@ -279,3 +279,23 @@ def test_host_api_returns_reference_tallies(golden):
         a, b = array("Q", bytes(8 * case["la"])), array("Q", bytes(8 * case["lb"]))
         x = array("Q", bytes(8 * (case["la"] + case["lb"] - 1)))
         assert list(k.multiply(a, b, x, p, top, K, (p + 1) // 2)) == case["tally"]
+
+
+@pytest.mark.parametrize("key", ["p998244353", "p3221225473", "p4179340454199820289"])
+def test_power_of_two_plus_r_against_oracle(golden, key):
+    """n = 2^k + r, r <= 4, beyond the cluster range: the 2^k transform plus r
+    dot products (p2r.cuh) -- both directions, single and batched."""
+    cfg = cfg_for(golden, key)
+    for n in [(1 << 18) + r for r in (1, 2, 3, 4)] + [(1 << 19) + 4, (1 << 18) + 5]:
+        x = gen(70_000 + n, cfg.p, n)
+        assert np.array_equal(run(T.tft, x, cfg), O.tft(x, cfg.p, cfg.omegaK, cfg.K)), n
+        z = gen(80_000 + n, cfg.p, n)
+        assert np.array_equal(run(T.itft, z, cfg), O.itft(z, cfg.p, cfg.omegaK, cfg.K)), n
+    n, cnt = (1 << 18) + 3, 3
+    flat = gen(90_001, cfg.p, n * cnt)
+    plan = device.BatchPlan(cfg, np.full(cnt, n))
+    d = device.to_words(flat, cfg)
+    plan.execute(d)
+    assert np.array_equal(device.from_words(d, cfg), O.tft_batch(flat, np.full(cnt, n), cfg.p, cfg.omegaK, cfg.K))
+    plan.execute(d, inverse=True)
+    assert np.array_equal(device.from_words(d, cfg), flat)
