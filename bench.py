@@ -409,21 +409,31 @@ def explore(args, T, device, backend, torch):
         i = _time(lambda: device.tft_batch_(d, cfg, n=1000, inverse=True), torch, args.steps * 20)
         out.append({"config": 1, "n": 1000, "fwd_us": f * 1e3, "inv_us": i * 1e3})
     elif args.config in (3, 5):
+        c3 = (1 << 24, (1 << 24) + 1, 3 << 23, (1 << 25) - 1, (1 << 25) + 1)
         if args.config == 3:
-            cases = [(3221225473, n) for n in (1 << 24, (1 << 24) + 1, 3 << 23, (1 << 25) - 1, (1 << 25) + 1)]
+            # BASELINE.md §3 resolution (p = 3221225473: 2^30 | p-1, canonical u32
+            # arithmetic), the same sizes at p = 469762049 = 7 2^26 + 1 (a p < 2^30
+            # prime like 998244353, lazy u32 arithmetic), and 998244353's own range
+            cases = [(3221225473, n) for n in c3] + [(469762049, n) for n in c3]
             cases += [(998244353, n) for n in (1 << 22, (1 << 22) + 1, 3 << 21, (1 << 23) - 1, 1 << 23)]
         else:
             ns = np.round(np.geomspace(1027, 268435451, 64)).astype(np.int64)
             ns = [int(n) + 1 if n & (n - 1) == 0 else int(n) for n in ns]
+            # u32 leg, then the u64 leg (p = 4179340454199820289)
             cases = [(998244353 if n <= (1 << 23) else 3221225473, n) for n in ns]
+            cases += [(4179340454199820289, n) for n in ns]
         for p, n in cases:
             cfg = T.config_for_modulus(p) if p != 998244353 else T.default_config()
             batch = max(1, (1 << 28) // n) if args.config == 5 else 1
             w = 4 if p < (1 << 32) else 8
             if batch * n * w > 6e9:
                 batch = max(1, int(6e9 // (n * w)))
-            d = torch.randint(0, 1 << 30, (batch * n,), dtype=torch.int32, device="cuda")
-            d.remainder_(p if p < (1 << 31) else (1 << 30))
+            if w == 4:
+                d = torch.randint(0, 1 << 30, (batch * n,), dtype=torch.int32, device="cuda")
+                d.remainder_(p if p < (1 << 31) else (1 << 30))
+            else:
+                d = torch.randint(0, 1 << 62, (batch * n,), dtype=torch.int64, device="cuda")
+                d.remainder_(p)
             plan = device.BatchPlan(cfg, np.full(batch, n))
             f = _time(lambda: plan.execute(d), torch, args.steps)
             i = _time(lambda: plan.execute(d, inverse=True), torch, args.steps)

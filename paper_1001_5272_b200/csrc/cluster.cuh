@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
                     const int64_t pos = (int64_t)j * C + head + (int64_t)q * NV;
                     if (q < nq && pos + NV <= nin) {
                         // the vector's other CTAs read the same rows: keep them in L2
-                        buf[u][j] = __ldg(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
+                        buf[u][j] = __ldcg(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
                     } else if (pos >= nin) {
                         buf[u][j] = Vec16<W>::zero();
                     } else {
