@@ -424,6 +424,7 @@ def explore(args, T, device, backend, torch):
             cases += [(4179340454199820289, n) for n in ns]
         for p, n in cases:
             cfg = T.config_for_modulus(p) if p != 998244353 else T.default_config()
+            sys.stdout.flush()
             batch = max(1, (1 << 28) // n) if args.config == 5 else 1
             w = 4 if p < (1 << 32) else 8
             if batch * n * w > 6e9:
@@ -434,7 +435,12 @@ def explore(args, T, device, backend, torch):
             else:
                 d = torch.randint(0, 1 << 62, (batch * n,), dtype=torch.int64, device="cuda")
                 d.remainder_(p)
-            plan = device.BatchPlan(cfg, np.full(batch, n))
+            try:
+                plan = device.BatchPlan(cfg, np.full(batch, n))
+            except Exception as e:  # e.g. u64 words beyond the two-pass range (2^26)
+                out.append({"config": args.config, "p": p, "n": n, "unsupported": str(e)})
+                del d
+                continue
             f = _time(lambda: plan.execute(d), torch, args.steps)
             i = _time(lambda: plan.execute(d, inverse=True), torch, args.steps)
             byt = batch * 2 * passes_min(n, w) * n * w
