@@ -178,12 +178,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     Scratch stash;
     if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
     a.stash = stash_buf ? stash_buf : (W*)stash.p;
-    constexpr int CL = Limits<F>::CL;
     const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
-    if (set_smem(k_chunk_fwd<F, CL>, sm_chunk) || set_smem(k_chunk_inv<F, CL>, sm_chunk) ||
-        set_smem(k_last_inv<F, CL>, sm_chunk))
-        return -1;
     // compile-time column kernels, one instantiation per l0
     void (*colf)(LaunchArgs<F>) = nullptr;
     void (*coli)(LaunchArgs<F>, int) = nullptr;
@@ -198,28 +194,39 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
 #undef TFTB_COL
         default: return fail("no column kernel for this plan");
     }
-    if (col_wlog<F, 4>() >= 0 && pl.wlog != std::max(0, std::min(8, Limits<F>::col_t - pl.l0)))
-        return fail("column plan mismatch");
+    if (pl.wlog != std::max(0, std::min(8, Limits<F>::col_t - pl.l0))) return fail("column plan mismatch");
     if (set_smem(colf, sm_col) || set_smem(coli, sm_col)) return -1;
-    for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
-        a.vbase = v0;
-        unsigned nv = (unsigned)std::min(count - v0, vchunk);
-        dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
-        if (!inverse) {
-            colf<<<gcol, kNT, sm_col, st>>>(a);
-            k_chunk_fwd<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
-            g_launches += 2;
-        } else {
-            static const int stop = getenv("TFTB_DEBUG_STOP") ? atoi(getenv("TFTB_DEBUG_STOP")) : 9;  // debug knob
-            if (stop >= 1) k_chunk_inv<F, CL><<<gchunk, kNT, sm_chunk, st>>>(a);
-            if (stop >= 2) coli<<<gcol, kNT, sm_col, st>>>(a, 0);
-            if (stop >= 3) k_last_inv<F, CL><<<glast, kNT, sm_chunk, st>>>(a);
-            if (stop >= 4) coli<<<gcol, kNT, sm_col, st>>>(a, 1);
-            g_launches += 4;
+    // chunk kernels for this plan's chunk size (2^CL, or 2^14 for the u64 words
+    // past 2^26, make_plan)
+    auto chunks = [&](auto cl) -> int {
+        constexpr int CLK = decltype(cl)::value;
+        if (set_smem(k_chunk_fwd<F, CLK>, sm_chunk) || set_smem(k_chunk_inv<F, CLK>, sm_chunk) ||
+            set_smem(k_last_inv<F, CLK>, sm_chunk))
+            return -1;
+        for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
+            a.vbase = v0;
+            unsigned nv = (unsigned)std::min(count - v0, vchunk);
+            dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
+            if (!inverse) {
+                colf<<<gcol, kNT, sm_col, st>>>(a);
+                k_chunk_fwd<F, CLK><<<gchunk, kNT, sm_chunk, st>>>(a);
+                g_launches += 2;
+            } else {
+                k_chunk_inv<F, CLK><<<gchunk, kNT, sm_chunk, st>>>(a);
+                coli<<<gcol, kNT, sm_col, st>>>(a, 0);
+                k_last_inv<F, CLK><<<glast, kNT, sm_chunk, st>>>(a);
+                coli<<<gcol, kNT, sm_col, st>>>(a, 1);
+                g_launches += 4;
+            }
+            CK(cudaGetLastError());
         }
-        CK(cudaGetLastError());
+        return 0;
+    };
+    if (pl.l1 == Limits<F>::CL) return chunks(std::integral_constant<int, Limits<F>::CL>{});
+    if constexpr (Limits<F>::CL < 14) {
+        if (pl.l1 == 14) return chunks(std::integral_constant<int, 14>{});
     }
-    return 0;
+    return fail("no chunk kernel for this plan");
 }
 
 // Build a reusable batch plan: vectors grouped by kernel plan, per-group
@@ -320,8 +327,9 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
         }
         Plan pl;
         make_plan<F>(g.maxn, &pl);
-        if (pl.kind == kLarge || pl.kind == kP2R)  // (p2r: its 2^k prefix runs the two-pass plan)
-            stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << Limits<F>::CL);
+        if (pl.kind == kLarge || pl.kind == kP2R)  // (p2r: its 2^k prefix runs the two-pass plan;
+            // chunks are 2^CL words, 2^14 for u64 words past 2^26)
+            stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << 14);
         g.arr_off = words;
         words += 2 * g.count;
         P->host_arrays.insert(P->host_arrays.end(), off.begin(), off.end());

@@ -152,9 +152,17 @@ int make_plan(int64_t n, Plan* pl, bool p2r_ok = true) {
     // rest, as many adjacent columns per CTA as fit a 2^col_t-word tile
     int l1 = CL;
     int l0 = l - l1;
+    int col_max = Limits<F>::col_t;
+    if (l0 > col_max && CL < 14) {
+        // u64 words past 2^26: 2^14-word (128 KB) chunk and column tiles, one
+        // CTA per SM -- slower per word, but it reaches 2^28 in two passes
+        l1 = 14;
+        l0 = l - l1;
+        col_max = 14;
+    }
     // up to 256 adjacent columns (colsum_pow needs blockDim >= columns)
     int wlog = std::max(0, std::min(8, Limits<F>::col_t - l0));
-    if (l0 + wlog > Limits<F>::col_t) return fail("transform length too large for the two-pass plan");
+    if (l0 + wlog > col_max) return fail("transform length too large for the two-pass plan");
     pl->l0 = l0;
     pl->l1 = l1;
     pl->wlog = wlog;

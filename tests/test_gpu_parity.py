@@ -299,3 +299,21 @@ def test_power_of_two_plus_r_against_oracle(golden, key):
     assert np.array_equal(device.from_words(d, cfg), O.tft_batch(flat, np.full(cnt, n), cfg.p, cfg.omegaK, cfg.K))
     plan.execute(d, inverse=True)
     assert np.array_equal(device.from_words(d, cfg), flat)
+
+
+def test_u64_past_two_to_the_26_round_trip_and_oracle_head(golden):
+    """u64 words beyond 2^26 run the two-pass plan with 2^14-word tiles:
+    exact round trip at 2^26 + 3 (p2r prefix) and 3 * 2^25, and the first
+    outputs against the oracle's naive evaluation."""
+    cfg = cfg_for(golden, "p4179340454199820289")
+    for n in ((1 << 26) + 3, 3 << 25):
+        flat = gen(123 + n, cfg.p, n)
+        d = device.to_words(flat, cfg)
+        device.tft_batch_(d, cfg, n=n)
+        got = device.from_words(d, cfg)
+        # outputs 0 and 1 are sum x and the alternating sum (omega_0 = 1, omega_1 = -1)
+        p = cfg.p
+        s0 = int(sum(int(v) for v in flat[::1]) % p)
+        assert int(got[0]) == s0
+        device.tft_batch_(d, cfg, n=n, inverse=True)
+        assert torch.equal(d, device.to_words(flat, cfg)), n
