@@ -1,24 +1,26 @@
-// One thread-block cluster per vector for 2^CL < n <= 8 * 2^CL (config 2's
-// 2^15 < n <= 2^16 lives here): CTA g of a G-CTA cluster owns chunk g =
-// positions [g*2^CL, (g+1)*2^CL) in shared memory, so a transform touches HBM
-// exactly once each way (BASELINE.md §5 passes_min = 1).
+// Vectors with 2^CL < n <= 8 * 2^CL (config 2's 2^15 < n <= 2^16 lives here)
+// are G = ceil(n / 2^CL) chunks of 2^CL words; chunk g = positions
+// [g 2^CL, (g+1) 2^CL).  A transform touches HBM once each way (BASELINE.md
+// §5 passes_min = 1).  The top gam = ceil_lg(n) - CL stages pair words in
+// different chunks: per column c (stride 2^CL) they are a 2^gam-point network.
 //
-// Forward: the top gam = ceil_lg(n) - CL stages of the network pair words in
-// different chunks; they run as 2^gam-point "column" transforms, one thread
-// per column reading and writing the G chunks through distributed shared
-// memory (columns are independent, so a column's owner thread is its only
-// reader and writer).  The remaining CL stages are local to each chunk (the
-// chunk is sub-block g of the network; its twiddles are the size-independent
-// omega_{2J} at global J).  Chunks past n are never materialised: their input
-// words are zero and their outputs are not needed.
+// Forward (k_clg_fwd, no cluster): CTA g reads the G rows of its columns
+// from global memory (the vector's first reader brings them from HBM, the
+// others hit L2), evaluates only row g's cone of each column network, then
+// the CL stages local to its chunk (sub-block g of the network: twiddles
+// omega_{2J} at global J).
 //
-// Inverse (K = n >> CL complete chunks, h = n mod 2^CL):
-//   1. chunks g < K: plain inverse of all CL local stages;
-//   2. columns c >= h: K known outputs -> K coefficients by V_K^-1, and the
-//      column's next output sum_j x_j omega_K^j written into chunk K slot c;
+// Inverse (k_cl_inv, one G-CTA cluster per vector; K = n >> CL complete
+// chunks, h = n mod 2^CL):
+//   1. chunks g < K: inverse of the CL local stages (left scaled by 2^CL);
+//      chunk K: phase 1 of its masked inverse;
+//   2. columns c >= h (over DSMEM): K known outputs -> K coefficients by
+//      V_K^-1 (REDC dot products; results straight to HBM), and the column's
+//      next output sum_j x_j omega_K^j into chunk K's slot c;
 //   3. chunk K: generalised in-tile inverse with h known outputs and the
 //      2^CL - h values from step 2 as its known tail;
 //   4. columns c < h: K+1 known outputs -> coefficients by V_{K+1}^-1.
+// The large path (n > 8 2^CL) uses the same split as two passes over HBM.
 // This is the two-level form of the inverse; values equal the
 // reference's Algorithm 2 because the inverse map is unique.
 #pragma once
@@ -340,97 +342,6 @@ __device__ __forceinline__ void col_share(uint32_t c0, uint32_t C, uint32_t g, u
     lo = c0 + ((uint32_t)(((uint64_t)span * g / G)) & ~31u);
     hi = g + 1 == G ? C : c0 + ((uint32_t)(((uint64_t)span * (g + 1) / G)) & ~31u);
     if (g == 0) lo = c0;
-}
-
-// the 2^GAM-point column network of the top GAM stages, one thread per column;
-// rows j >= G are past n (zero in, dropped out)
-template <class F, int GAM>
-TFT_DEV void cross_fwd(const F& f, cg::cluster_group& cl, typename F::W* S, uint32_t g, uint32_t G, uint32_t C,
-                       const Tw<typename F::W>* Zw) {
-    using W = typename F::W;
-    constexpr int GP = 1 << GAM;
-    W* rs[GP];
-#pragma unroll
-    for (int j = 0; j < GP; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
-    Tw<W> tw[GP / 2 > 0 ? GP / 2 : 1];
-#pragma unroll
-    for (int j = 0; j < GP / 2; ++j) tw[j] = ldg_tw(Zw + j);
-    uint32_t lo, hi;
-    col_share(0, C, g, G, lo, hi);
-    // UNR columns per thread in flight: DSMEM loads are ~200+ cycles each
-    constexpr int UNR = GP <= 2 ? 8 : (GP <= 4 ? 4 : 2);
-    for (uint32_t c0 = lo + threadIdx.x; c0 < hi; c0 += blockDim.x * UNR) {
-        W col[UNR][GP];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t c = c0 + u * blockDim.x;
-            const uint32_t ph = c + (c >> 5);
-#pragma unroll
-            for (int j = 0; j < GP; ++j) col[u][j] = (j < (int)G && c < hi) ? rs[j][ph] : W(0);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-#pragma unroll
-            for (int sp = GAM - 1; sp >= 0; --sp) {
-#pragma unroll
-                for (int j = 0; j < GP; ++j) {
-                    if ((j >> sp) & 1) continue;
-                    f.fwd(col[u][j], col[u][j + (1 << sp)], tw[j >> (sp + 1)]);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const uint32_t c = c0 + u * blockDim.x;
-            if (c >= hi) break;
-            const uint32_t ph = c + (c >> 5);
-#pragma unroll
-            for (int j = 0; j < GP; ++j)
-                if (j < (int)G) rs[j][ph] = col[u][j];
-        }
-    }
-}
-
-// ------------------------------------------------------------ kernels
-template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
-__global__ void __launch_bounds__(NT, MINB) k_cl_fwd(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    W* S = reinterpret_cast<W*>(smem_raw);
-    cg::cluster_group cl = cg::this_cluster();
-    const uint32_t g = cl.block_rank(), G = cl.num_blocks();
-    constexpr uint32_t C = 1u << CL;
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
-    const int gam = ceil_lg_dev(n) - CL;
-    W* x = a.x + a.xd.o(v);
-    const W* in = a.in + a.ind.o(v);
-    const F f = a.f;
-
-    const int64_t cbase = (int64_t)g * C;
-    TFTB_STAMP(a, 0);
-    tile_load<W>(S, in + cbase, nin - cbase, C, [](uint32_t, W w) { return w; });
-    TFTB_STAMP(a, 1);
-    cl.sync();
-    TFTB_STAMP(a, 2);
-
-    // cross stages: 2^gam-point untwisted column transforms over DSMEM
-    switch (gam) {
-        case 1: cross_fwd<F, 1>(f, cl, S, g, G, C, a.R.Zf); break;
-        case 2: cross_fwd<F, 2>(f, cl, S, g, G, C, a.R.Zf); break;
-        default: cross_fwd<F, 3>(f, cl, S, g, G, C, a.R.Zf); break;
-    }
-    TFTB_STAMP(a, 3);
-    cl.sync();
-    TFTB_STAMP(a, 4);
-
-    // only this chunk's rows below n are outputs: prune the rest
-    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f, a.R.ZfM}, (uint32_t)min((int64_t)C, n - cbase));
-    TFTB_STAMP(a, 5);
-
-    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
-    tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
-    TFTB_STAMP(a, 6);
 }
 
 // dot product of M canonical words with M Montgomery words, reduced once:

@@ -128,9 +128,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
         const int nt = kNT;
-        auto kf = k_cl_fwd<F, CL>;
         auto ki = k_cl_inv<F, CL>;
-        if (set_smem(kf, smem) || set_smem(ki, smem)) return -1;
+        if (set_smem(ki, smem)) return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
@@ -146,11 +145,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            static const bool dsmem_fwd = getenv("TFTB_FWD_DSMEM") != nullptr;  // A/B knob
             if (inverse) {
                 CK(cudaLaunchKernelEx(&lc, ki, a));
-            } else if (dsmem_fwd) {
-                CK(cudaLaunchKernelEx(&lc, kf, a));
             } else {
                 // no-cluster forward: rows re-read through L2 instead of DSMEM
                 const int gam = pl.l - CL;
@@ -189,7 +185,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         colf = k_colc_fwd<F, L>;        \
         coli = k_colc_inv<F, L>;        \
         break;
-        TFTB_COL(1) TFTB_COL(2) TFTB_COL(3) TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
+        TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
         TFTB_COL(10) TFTB_COL(11) TFTB_COL(12) TFTB_COL(13) TFTB_COL(14)
 #undef TFTB_COL
         default: return fail("no column kernel for this plan");

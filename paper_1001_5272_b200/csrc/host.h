@@ -135,8 +135,7 @@ int make_plan(int64_t n, Plan* pl, bool p2r_ok = true) {
         pl->kind = kSmall;
         return 0;
     }
-    static const bool no_cluster = getenv("TFTB_NO_CLUSTER") != nullptr;  // A/B knob
-    if (n <= (8ll << CL) && !no_cluster) {
+    if (n <= (8ll << CL)) {
         pl->kind = kCluster;
         pl->G = (int)((n + (1ll << CL) - 1) >> CL);
         return 0;

@@ -156,85 +156,6 @@ __device__ __forceinline__ int ceil_lg_dev(int64_t n) {
     return n <= 1 ? 0 : 64 - __clzll((unsigned long long)(n - 1));
 }
 
-// ------------------------------------------------------------ two-pass, forward
-// grid: (C >> wlog column groups, vectors)
-template <class F>
-__global__ void k_col_fwd(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    W* S = reinterpret_cast<W*>(smem_raw);
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
-    const int l1 = a.l1, l0 = ceil_lg_dev(n) - l1;
-    if (l0 <= 0) return;
-    const uint32_t C = 1u << l1, c0 = blockIdx.x << a.wlog, ncols = 1u << a.wlog;
-    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
-    W* x = a.x + a.xd.o(v);
-    const W* in = a.in + a.ind.o(v);
-    SmemTile<W> tl{S, l0, a.wlog};
-    const uint32_t words = tl.words();
-    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
-        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
-        int64_t pos = (int64_t)row * C + c0 + col;
-        tl.at(g) = pos < nin ? in[pos] : W(0);
-    }
-    __syncthreads();
-    fwd_all(a.f, tl, TwPrefix<F>{a.R.Zf});
-    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
-        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
-        int64_t pos = (int64_t)row * C + c0 + col;
-        if (pos < n) x[pos] = a.f.canon(tl.at(g));
-        else if (h && row == K) a.stash[(v - a.vbase) * (int64_t)C + c0 + col] = a.f.canon(tl.at(g));
-    }
-}
-
-// ------------------------------------------------------------ two-pass, inverse
-// steps 2 (which = 0: columns c >= h, K rows, stash their row K) and
-// 4 (which = 1: columns c < h, K+1 rows).  grid: (C >> wlog, vectors)
-template <class F>
-__global__ void k_col_inv(LaunchArgs<F> a, int which) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v);
-    const int l1 = a.l1, l0 = ceil_lg_dev(n) - l1;
-    if (l0 <= 0) return;
-    const uint32_t C = 1u << l1, c0 = blockIdx.x << a.wlog, ncols = 1u << a.wlog;
-    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
-    // column range of this step
-    const uint32_t lo = which == 0 ? h : 0, hi = which == 0 ? C : h;
-    if (c0 + ncols <= lo || c0 >= hi) return;
-    const uint32_t rows = which == 0 ? K : K + 1;
-    W* S = reinterpret_cast<W*>(smem_raw);
-    SmemTile<W> tl{S, l0, a.wlog};
-    W* red = S + padded_words(tl.words());
-    W* nv = red + blockDim.x;
-    const int64_t o = a.xd.o(v);
-    W* x = a.x + o;
-    const uint32_t words = tl.words();
-    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
-        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
-        int64_t pos = (int64_t)row * C + c0 + col;
-        tl.at(g) = (row < rows && pos < n) ? x[pos] : W(0);
-    }
-    __syncthreads();
-    itft_gen(a.f, tl, rows, TwPrefix<F>{a.R.Zf}, TwPrefix<F>{a.R.Zi}, a.R);
-    for (uint32_t g = threadIdx.x; g < words; g += blockDim.x) {
-        uint32_t col = g & (ncols - 1), row = g >> a.wlog;
-        uint32_t c = c0 + col;
-        int64_t pos = (int64_t)row * C + c;
-        if (row < rows && c >= lo && c < hi && pos < n) x[pos] = a.f.canon(tl.at(g));
-    }
-    if (which == 0 && h) {
-        // the column's first virtual output z_c[K] = sum_{i<K} x_i omega_K^i
-        colsum_pow(a.f, tl, K, omega_w(a.f, a.R, K), a.R.oneW, red, nv);
-        for (uint32_t col = threadIdx.x; col < ncols; col += blockDim.x) {
-            uint32_t c = c0 + col;
-            if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
-        }
-    }
-}
-
 // ------------------------------------------------------------ helpers
 template <typename W>
 __global__ void k_u64_to_w(const uint64_t* __restrict__ s, W* __restrict__ d, int64_t n) {

@@ -159,116 +159,6 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
     if constexpr (ST + 1 < KK) reg_inv<F, KK, ST + 1, MASK>(f, v, base, slo, tp, h, last, ipow2);
 }
 
-// ---------------------------------------------------------------- rounds
-template <class F, int KK, class TP>
-TFT_DEV void fwd_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, const TP& tp) {
-    using W = typename F::W;
-    const uint32_t cmask = (1u << tl.wlog) - 1;
-    const uint32_t nunits = 1u << (tl.t - KK + tl.wlog);
-    const uint32_t lomask = (1u << s_lo) - 1;
-    for (uint32_t g = threadIdx.x; g < nunits; g += blockDim.x) {
-        uint32_t col = g & cmask, u = g >> tl.wlog;
-        uint32_t base = (u & lomask) | ((u >> s_lo) << (s_lo + KK));
-        W v[1 << KK];
-#pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
-        reg_fwd<F, KK, KK - 1>(f, v, base, s_lo, tp);
-#pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
-    }
-}
-
-// Inverse round, stages s_lo .. s_lo+KK-1 ascending.  With MASK, only pairs
-// inside complete aligned 2^(s+1)-blocks of [0, h) run, and a pair in its
-// block's last stage (u >= h rounded down to 2^(s+2)) is scaled by 2^-(s+1)
-// so every complete block leaves phase 1 holding true (unscaled) values.
-// Without MASK the whole tile is one block and the scale lands at s = t-1.
-template <class F, int KK, bool MASK, class TP>
-TFT_DEV void inv_round(const F& f, const SmemTile<typename F::W>& tl, int s_lo, const TP& tp,
-                       uint32_t h, const Tw<typename F::W>* ipow2) {
-    using W = typename F::W;
-    const uint32_t cmask = (1u << tl.wlog) - 1;
-    const uint32_t nunits = 1u << (tl.t - KK + tl.wlog);
-    const uint32_t lomask = (1u << s_lo) - 1;
-    const uint32_t h_lo = MASK ? ((uint32_t)((uint64_t)h >> (s_lo + 1)) << (s_lo + 1)) : 0;
-    for (uint32_t g = threadIdx.x; g < nunits; g += blockDim.x) {
-        uint32_t col = g & cmask, u = g >> tl.wlog;
-        uint32_t base = (u & lomask) | ((u >> s_lo) << (s_lo + KK));
-        if (MASK && base >= h_lo) continue;  // no pair of this unit is active in any stage
-        W v[1 << KK];
-#pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) v[i] = tl.at(tl.ix(base + ((uint32_t)i << s_lo), col));
-        reg_inv<F, KK, 0, MASK>(f, v, base, s_lo, tp, h, tl.t - 1, ipow2);
-#pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) tl.at(tl.ix(base + ((uint32_t)i << s_lo), col)) = v[i];
-    }
-}
-
-template <class F, class TP>
-TFT_DEV void fwd_round_rt(const F& f, const SmemTile<typename F::W>& tl, int s_lo, int kk, const TP& tp) {
-    switch (kk) {
-        case 1: fwd_round<F, 1>(f, tl, s_lo, tp); break;
-        case 2: fwd_round<F, 2>(f, tl, s_lo, tp); break;
-        case 3: fwd_round<F, 3>(f, tl, s_lo, tp); break;
-        case 4: fwd_round<F, 4>(f, tl, s_lo, tp); break;
-        default: fwd_round<F, 5>(f, tl, s_lo, tp); break;
-    }
-}
-
-template <class F, bool MASK, class TP>
-TFT_DEV void inv_round_rt(const F& f, const SmemTile<typename F::W>& tl, int s_lo, int kk,
-                          const TP& tp, uint32_t h, const Tw<typename F::W>* ipow2) {
-    switch (kk) {
-        case 1: inv_round<F, 1, MASK>(f, tl, s_lo, tp, h, ipow2); break;
-        case 2: inv_round<F, 2, MASK>(f, tl, s_lo, tp, h, ipow2); break;
-        case 3: inv_round<F, 3, MASK>(f, tl, s_lo, tp, h, ipow2); break;
-        case 4: inv_round<F, 4, MASK>(f, tl, s_lo, tp, h, ipow2); break;
-        default: inv_round<F, 5, MASK>(f, tl, s_lo, tp, h, ipow2); break;
-    }
-}
-
-// Full forward transform of every column (all t stages).  Caller has synced
-// after filling the tile; ends synced.
-template <class F, class TP>
-TFT_DEV void fwd_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp) {
-    const int t = tl.t;
-    const int last = t < 5 ? t : 5;
-    int s_hi = t;
-    int first = (t - last) & 3;
-    if (first) {
-        fwd_round_rt(f, tl, s_hi - first, first, tp);
-        s_hi -= first;
-        __syncthreads();
-    }
-    while (s_hi > last) {
-        fwd_round_rt(f, tl, s_hi - 4, 4, tp);
-        s_hi -= 4;
-        __syncthreads();
-    }
-    if (last) {
-        fwd_round_rt(f, tl, 0, last, tp);
-        __syncthreads();
-    }
-}
-
-template <class F, bool MASK, class TP>
-TFT_DEV void inv_all(const F& f, const SmemTile<typename F::W>& tl, const TP& tp, uint32_t h,
-                     const Tw<typename F::W>* ipow2) {
-    const int t = tl.t;
-    const int first = t < 5 ? t : 5;
-    if (first) {
-        inv_round_rt<F, MASK>(f, tl, 0, first, tp, h, ipow2);
-        __syncthreads();
-    }
-    int s_lo = first;
-    while (s_lo < t) {
-        int kk = t - s_lo < 4 ? t - s_lo : 4;
-        inv_round_rt<F, MASK>(f, tl, s_lo, kk, tp, h, ipow2);
-        s_lo += kk;
-        __syncthreads();
-    }
-}
-
 // Generalised in-tile inverse (every column at once): slots [0, h) hold
 // transform outputs, slots [h, 2^t) hold KNOWN coefficients (zeros for a plain
 // ITFT, stashed virtual values for the last chunk of a two-pass ITFT).  On
@@ -363,13 +253,6 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
         }
         __syncthreads();
     }
-}
-
-template <class F, class TPF, class TPI>
-TFT_DEV void itft_gen(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
-                      const TPI& tpi, const RingDev<typename F::W>& R) {
-    inv_all<F, true>(f, tl, tpi, h, R.ipow2);
-    itft_phases23(f, tl, h, tpf, tpi, R);
 }
 
 // Per-column evaluation sum_{i<K} S[i] w^i (the first virtual output of a
