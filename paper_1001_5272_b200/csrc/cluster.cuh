@@ -4,11 +4,12 @@
 // §5 passes_min = 1).  The top gam = ceil_lg(n) - CL stages pair words in
 // different chunks: per column c (stride 2^CL) they are a 2^gam-point network.
 //
-// Forward (k_clg_fwd, no cluster): CTA g reads the G rows of its columns
-// from global memory (the vector's first reader brings them from HBM, the
-// others hit L2), evaluates only row g's cone of each column network, then
-// the CL stages local to its chunk (sub-block g of the network: twiddles
-// omega_{2J} at global J).
+// Forward (k_clg_fwd, one G-CTA cluster per vector, no DSMEM): CTA g reads
+// the G rows of its columns from global memory (the vector's first reader
+// brings them from HBM, the others hit L2), evaluates only row g's cone of
+// each column network, then the CL stages local to its chunk (sub-block g of
+// the network: twiddles omega_{2J} at global J).  A split cluster barrier
+// keeps every chunk store behind all siblings' row reads (in place).
 //
 // Inverse (k_cl_inv, one G-CTA cluster per vector; K = n >> CL complete
 // chunks, h = n mod 2^CL):
@@ -35,6 +36,10 @@ template <class F>
 constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : 3; }
 
 namespace cg = cooperative_groups;
+
+// split cluster barrier (every thread of the CTA arrives / waits)
+TFT_DEV void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+TFT_DEV void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
 // read-only load of one twiddle pair
 template <typename W>
@@ -725,14 +730,15 @@ __global__ void __launch_bounds__(256) k_colc_inv(LaunchArgs<F> a, int which) {
     }
 }
 
-// ===================================== forward for 2^CL < n <= 8 2^CL, no cluster
+// ============================ forward for 2^CL < n <= 8 2^CL, no DSMEM
 // CTA g of vector v needs row g of every column's 2^GAM-point network.  It
 // reads the column's rows straight from global memory (the first CTA of a
 // vector brings them from HBM, its siblings hit L2) and evaluates only the
 // cone of row g: the top stage has theta = 1 (adds only), stage sp keeps the
 // half selected by bit sp of g with one twiddle omega_{2 (g >> (sp+1))}, so a
-// word costs at most GAM-1 products (<= 1 for config 2).  No DSMEM, no
-// cluster barrier; grid (G, vectors).
+// word costs at most GAM-1 products (<= 1 for config 2).  No DSMEM; grid
+// (G, vectors) in clusters of G, whose only use is the split barrier that
+// orders the in-place chunk stores after the siblings' row reads.
 template <class F, int GAM>
 TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, const Tw<typename F::W>* tw) {
     using W = typename F::W;
@@ -767,7 +773,11 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
     const int64_t v = a.vbase + blockIdx.y;
     const int64_t n = a.xd.n(v), nin = a.ind.n(v);
     const int64_t cbase = (int64_t)g * C;
-    if (cbase >= n) return;
+    if (cbase >= n) {  // (never for a plan's vectors) still takes part in the cluster barrier
+        cluster_arrive_release();
+        cluster_wait_acquire();
+        return;
+    }
     const F f = a.f;
     W* x = a.x + a.xd.o(v);
     const W* in = a.in + a.ind.o(v);
@@ -830,10 +840,17 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
         for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
     }
     TFTB_STAMP(a, 1);
+    // In place (in == x), chunk g is also a row of every sibling CTA's
+    // columns: this CTA's reads are done, and it may not overwrite its chunk
+    // before every sibling has signalled the same.  The vector's G CTAs are
+    // one cluster (co-scheduled), so the split barrier cannot deadlock, and
+    // the rounds below hide its latency.
+    cluster_arrive_release();
     __syncthreads();
     TFTB_STAMP(a, 2);
     fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f, a.R.ZfM}, (uint32_t)min((int64_t)C, n - cbase));
     TFTB_STAMP(a, 5);
+    cluster_wait_acquire();
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     tile_store<W>(x + cbase, S, lim, [&](W w) { return f.canon(w); });
     TFTB_STAMP(a, 6);

@@ -148,13 +148,12 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             if (inverse) {
                 CK(cudaLaunchKernelEx(&lc, ki, a));
             } else {
-                // no-cluster forward: rows re-read through L2 instead of DSMEM
+                // forward: rows re-read through L2 instead of DSMEM (cluster only for the store barrier)
                 const int gam = pl.l - CL;
                 void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
                                            : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
                 if (set_smem(kg, smem)) return -1;
-                kg<<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
-                CK(cudaGetLastError());
+                CK(cudaLaunchKernelEx(&lc, kg, a));
             }
             g_launches++;
         }
