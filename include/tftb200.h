@@ -108,6 +108,14 @@ const char* tftb_last_error(void);
 const char* tftb_version(void);
 /* Number of kernel launches issued by this thread since the last reset. */
 int64_t tftb_launch_count(int reset);
+/* Footprint audit (the device analogue of the reference's audited_call,
+ * oracle.py:118-137): high-water mark of the device bytes this thread's
+ * calls allocated beyond the transformed words themselves (two-pass stash,
+ * p2r partial sums, the product's second operand) since the last reset.
+ * Host-API staging of the caller's own words is not counted.  0 for every
+ * transform with n <= 2^17 (u32 words): the tile and cluster plans run in
+ * the n-word buffer alone. */
+int64_t tftb_aux_bytes(int reset);
 
 /* ------------------------------------------------------------ op tallies
  * (mults, adds) the reference walk reports for the same call: the second

@@ -59,6 +59,7 @@ SIGNATURES = {
     "tftb_last_error": (ctypes.c_char_p, []),
     "tftb_version": (ctypes.c_char_p, []),
     "tftb_launch_count": (ctypes.c_int64, [ctypes.c_int]),
+    "tftb_aux_bytes": (ctypes.c_int64, [ctypes.c_int]),
     "tftb_tally_transform": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _i64p, _i64p]),
     "tftb_tally_multiply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, _i64p,
                                            _i64p]),
@@ -165,3 +166,9 @@ def ring_handle(cfg):
 
 def launch_count(reset=False):
     return int(load().tftb_launch_count(1 if reset else 0))
+
+
+def aux_bytes(reset=False):
+    """Device bytes this thread's calls allocated beyond the transformed
+    words (high-water mark since the last reset): the footprint audit."""
+    return int(load().tftb_aux_bytes(1 if reset else 0))

@@ -171,7 +171,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     const int64_t maxchunks = (maxn + C - 1) / C;
     const int64_t vchunk = 65535;
     Scratch stash;
-    if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st)) return -1;
+    if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st, true)) return -1;
     a.stash = stash_buf ? stash_buf : (W*)stash.p;
     const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
@@ -242,7 +242,7 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
     const int64_t vchunk = 65535;
     const int64_t cmax = std::min(count, vchunk);
     Scratch part;
-    if (part.get((size_t)cmax * nb * kP2RMax * sizeof(W) + (size_t)cmax * sizeof(unsigned), st)) return -1;
+    if (part.get((size_t)cmax * nb * kP2RMax * sizeof(W) + (size_t)cmax * sizeof(unsigned), st, true)) return -1;
     unsigned* ticket = reinterpret_cast<unsigned*>((W*)part.p + (size_t)cmax * nb * kP2RMax);
     CK(cudaMemsetAsync(ticket, 0, (size_t)cmax * sizeof(unsigned), st));
     P2RConsts<F> c{};
@@ -384,7 +384,7 @@ int dispatch_mul(const RingHost* rh, const void* a, int64_t la, int64_t sa, cons
     if (sx != r) return fail("multiply_dev: output stride must equal la+lb-1");
     Scratch own;
     if (!scratch) {
-        if (own.get((size_t)count * r * sizeof(W), st)) return -1;
+        if (own.get((size_t)count * r * sizeof(W), st, true)) return -1;
         scratch = own.p;
     }
     // X_v <- TFT_r(a_v || 0), Y_v <- TFT_r(b_v || 0), X_v <- ITFT_r(X_v * Y_v)

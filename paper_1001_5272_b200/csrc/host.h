@@ -24,6 +24,10 @@ typedef unsigned __int128 u128;
 
 extern thread_local std::string g_err;
 extern thread_local int64_t g_launches;
+// device bytes a transform allocates beyond its own n words (stash, p2r
+// partials, the product's second operand): current and high-water mark of
+// this thread's calls -- the footprint audit (tftb_aux_bytes)
+extern thread_local int64_t g_aux_cur, g_aux_peak;
 
 inline int fail(const std::string& msg) {
     g_err = msg;
@@ -187,16 +191,25 @@ int set_smem(K_ kern, size_t bytes) {
 struct Scratch {
     void* p = nullptr;
     size_t bytes = 0;
+    bool aux = false;
     cudaStream_t s = nullptr;
-    int get(size_t b, cudaStream_t st) {
+    // aux: auxiliary space of the algorithm (counted by the footprint audit),
+    // as opposed to host-API staging of the caller's own words
+    int get(size_t b, cudaStream_t st, bool is_aux = false) {
         s = st;
         if (b == 0) return 0;
         CK(cudaMallocAsync(&p, b, st));
         bytes = b;
+        aux = is_aux;
+        if (aux) {
+            g_aux_cur += (int64_t)b;
+            g_aux_peak = std::max(g_aux_peak, g_aux_cur);
+        }
         return 0;
     }
     ~Scratch() {
         if (p) cudaFreeAsync(p, s);
+        if (p && aux) g_aux_cur -= (int64_t)bytes;
     }
 };
 

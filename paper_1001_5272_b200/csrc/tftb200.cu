@@ -22,6 +22,7 @@ namespace tftb {
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+thread_local int64_t g_aux_cur = 0, g_aux_peak = 0;
 
 template <typename W>
 struct TableBuilder {
@@ -561,6 +562,12 @@ const char* tftb_version(void) { return "tftb200 0.1.0 (sm_100a)"; }
 int64_t tftb_launch_count(int reset) {
     int64_t v = g_launches;
     if (reset) g_launches = 0;
+    return v;
+}
+
+int64_t tftb_aux_bytes(int reset) {
+    const int64_t v = g_aux_peak;
+    if (reset) g_aux_peak = g_aux_cur;
     return v;
 }
 

@@ -28,3 +28,5 @@ def test_version_and_counters():
     lib = backend.load()
     assert b"sm_100a" in lib.tftb_version()
     assert backend.launch_count(reset=True) >= 0
+    backend.aux_bytes(reset=True)
+    assert backend.aux_bytes() == 0  # nothing allocated without a call

@@ -317,3 +317,29 @@ def test_u64_past_two_to_the_26_round_trip_and_oracle_head(golden):
         assert int(got[0]) == s0
         device.tft_batch_(d, cfg, n=n, inverse=True)
         assert torch.equal(d, device.to_words(flat, cfg)), n
+
+
+@pytest.mark.gpu
+def test_device_footprint_audit():
+    """The in-place claim on device: tile and cluster plans (n <= 2^17 u32)
+    allocate nothing beyond the n words; larger transforms at most a stash
+    of one chunk (2^14 words) per vector plus p2r partial sums -- O(sqrt n),
+    independent of n."""
+    import numpy as np
+    import paper_1001_5272_b200 as T
+    from paper_1001_5272_b200 import backend
+    cfg = T.default_config()
+    for n in (16, 512, 5000, 40000, 131072):
+        x = np.random.default_rng(n).integers(0, cfg.p, n, dtype=np.uint64)
+        backend.aux_bytes(reset=True)
+        T.tft(x, cfg)
+        T.itft(x, cfg)
+        assert backend.aux_bytes() == 0, n
+    peaks = []
+    for n in (2 ** 18 + 7, 2 ** 20 + 1, 2 ** 21 - 3, 3 * 2 ** 21):
+        x = np.random.default_rng(n).integers(0, cfg.p, n, dtype=np.uint64)
+        backend.aux_bytes(reset=True)
+        T.tft(x, cfg)
+        T.itft(x, cfg)
+        peaks.append(backend.aux_bytes())
+    assert max(peaks) <= 2 ** 14 * 4 + 4096, peaks
