@@ -72,8 +72,10 @@ int tftb_ring_word_bytes(const tftb_ring* ring);
  * one device buffer `data` (ring word type).  Vector v starts at word
  * h_off[v] (or v*stride when h_off == NULL) and has length h_len[v] (or n
  * when h_len == NULL).  h_off/h_len are HOST arrays.  Vectors must not
- * overlap.  `stream` is a cudaStream_t (NULL = legacy default stream).
- * Asynchronous w.r.t. the host. */
+ * overlap.  Words are canonical residues (< p), as everywhere in the
+ * reference (modring.py:408-422); outputs are canonical.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Asynchronous w.r.t. the
+ * host. */
 int tftb_tft_dev(const tftb_ring* ring, void* data, int64_t count, int64_t n, int64_t stride,
                  const int64_t* h_off, const int64_t* h_len, int inverse, void* stream);
 

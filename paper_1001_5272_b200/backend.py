@@ -22,7 +22,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtftb200.so")
+# TFTB_LIB: an alternative build of the same library (tools/build_variant.py experiments)
+LIB_PATH = os.environ.get("TFTB_LIB") or os.path.join(_HERE, "libtftb200.so")
 
 _forced = os.environ.get("TFTMUL_BACKEND", "").strip().lower()
 if _forced in ("py", "pure", "python"):

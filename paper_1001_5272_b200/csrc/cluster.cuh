@@ -27,13 +27,17 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#ifndef TFTB_MINB32
+#define TFTB_MINB32 3
+#endif
+
 #include "kernels.cuh"
 #include <type_traits>
 
 // CTAs per SM the 256-thread tile kernels are compiled for: 3 (80 registers)
 // for u32 words; u64 words need twice the registers per 32-word unit, so 2
 template <class F>
-constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : 3; }
+constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : TFTB_MINB32; }
 
 namespace cg = cooperative_groups;
 
@@ -455,6 +459,71 @@ TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg
     }
 }
 
+// The last chunk's second column solve, columns [0, h) with M = K + 1 rows:
+// rows j < K come from global memory (L2: the complete chunks published
+// them), row K from this CTA's tile.  u32 words: 4 adjacent columns per
+// thread with 16-byte loads and stores (every row shares the vector's
+// 16-byte alignment, C being a multiple of 4) and 2 quads in flight, so the
+// L2 round trips are 8x fewer than with scalar loads; ragged head and tail
+// columns go through col_solve_range.
+template <class F, int M>
+TFT_DEV void col2_quads(const F& f, typename F::W* x, const typename F::W* S, uint32_t C, uint32_t h,
+                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
+    using W = typename F::W;
+    constexpr int K = M - 1, QIF = M <= 3 ? 2 : 1;
+    auto ld = [&](int j, uint32_t c) { return (uint32_t)j < (uint32_t)K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
+    auto nx = [](uint32_t, W) {};
+    const uint32_t mis = (uint32_t)(((uintptr_t)x & 15) / sizeof(W));
+    const uint32_t head = min(h, (4 - mis) & 3);
+    const uint32_t nq = (h - head) / 4, body_end = head + 4 * nq;
+    if (head) col_solve_range<F, M>(f, ld, nx, x, C, 0, head, blk, blkM, false);
+    for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += QIF * blockDim.x) {
+        uint4 r[QIF][K];
+#pragma unroll
+        for (int u = 0; u < QIF; ++u) {
+            const uint32_t c0 = head + 4 * (q0 + u * blockDim.x);
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (q0 + u * blockDim.x < nq) r[u][j] = __ldcg(reinterpret_cast<const uint4*>(x + (size_t)j * C + c0));
+        }
+#pragma unroll
+        for (int u = 0; u < QIF; ++u) {
+            const uint32_t c0 = head + 4 * (q0 + u * blockDim.x);
+            if (q0 + u * blockDim.x >= nq) break;
+            W out[M][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                W y[M], xv[M];
+#pragma unroll
+                for (int j = 0; j < K; ++j) y[j] = k == 0 ? r[u][j].x : k == 1 ? r[u][j].y : k == 2 ? r[u][j].z : r[u][j].w;
+                const uint32_t c = c0 + k;
+                y[K] = S[c + (c >> 5)];
+                col_solve_vals<F, M>(f, y, blk, blkM, xv, nullptr);
+#pragma unroll
+                for (int j = 0; j < M; ++j) out[j][k] = xv[j];
+            }
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+                *reinterpret_cast<uint4*>(x + (size_t)j * C + c0) = make_uint4(out[j][0], out[j][1], out[j][2], out[j][3]);
+        }
+    }
+    if (body_end < h) col_solve_range<F, M>(f, ld, nx, x, C, body_end, h, blk, blkM, false);
+}
+
+template <class F>
+TFT_DEV void col2_solve(const F& f, typename F::W* x, const typename F::W* S, uint32_t C, uint32_t h, int m,
+                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
+    switch (m) {
+        case 2: col2_quads<F, 2>(f, x, S, C, h, blk, blkM); break;
+        case 3: col2_quads<F, 3>(f, x, S, C, h, blk, blkM); break;
+        case 4: col2_quads<F, 4>(f, x, S, C, h, blk, blkM); break;
+        default: {  // (G > 4: few vectors; registers would spill) scalar loads
+            auto ld = [&](int j, uint32_t c) { return (uint32_t)j < (uint32_t)(m - 1) ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
+            col_solve(f, ld, [](uint32_t, typename F::W) {}, x, C, 0, h, m, blk, blkM, false);
+        }
+    }
+}
+
 template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
 __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;
@@ -516,9 +585,14 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     }
     TFTB_STAMP(a, 6);
     // columns < h: K + 1 rows, K of them from the complete chunks
-    col_solve(
-        f, [&](int j, uint32_t c) { return (uint32_t)j < K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; },
-        [](uint32_t, W) {}, x, C, 0, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
+#ifndef TFTB_COL2_SCALAR
+    if constexpr (sizeof(W) == 4)
+        col2_solve(f, x, S, C, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K);
+    else
+#endif
+        col_solve(
+            f, [&](int j, uint32_t c) { return (uint32_t)j < K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; },
+            [](uint32_t, W) {}, x, C, 0, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
     TFTB_STAMP(a, 7);
 }
 
@@ -743,6 +817,32 @@ template <class F, int GAM>
 TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, const Tw<typename F::W>* tw) {
     using W = typename F::W;
     constexpr int GP = 1 << GAM;
+#ifndef TFTB_CONE_GENERIC
+    if constexpr (F::kLazy) {
+        // inputs are canonical residues: the top stage (theta = 1) gives
+        // [0, 2p) without a reduction, so does the second stage's left
+        // operand; later stages reduce it from [0, 4p)
+        {
+            constexpr int H = GP / 2;
+            const bool sel = (g >> (GAM - 1)) & 1;
+#pragma unroll
+            for (int i = 0; i < H; ++i) vals[i] = sel ? vals[i] - vals[i + H] + f.p : vals[i] + vals[i + H];
+        }
+#pragma unroll
+        for (int sp = GAM - 2; sp >= 0; --sp) {
+            const int H = 1 << sp;
+            const bool sel = (g >> sp) & 1;
+            const Tw<W> t = tw[sp];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const W a = sp == GAM - 2 ? vals[i] : f.red2(vals[i]);
+                const W b = f.mulw(vals[i + H], t);
+                vals[i] = sel ? a - b + f.p2 : a + b;
+            }
+        }
+        return vals[0];
+    }
+#endif
     // top stage: theta = 1
     {
         constexpr int H = GP / 2;
@@ -761,8 +861,14 @@ TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, cons
     return vals[0];
 }
 
+#ifndef TFTB_CLG_NT
+#define TFTB_CLG_NT 256
+#endif
+#ifndef TFTB_CLG_MINB
+#define TFTB_CLG_MINB kern_minb<F>()
+#endif
 template <class F, int CL, int GAM>
-__global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(TFTB_CLG_NT, TFTB_CLG_MINB) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
@@ -800,7 +906,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
     };
     for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
     {
-        constexpr int UNR = GP <= 4 ? 2 : 1;
+        constexpr int UNR = GP <= 4 ? TFTB_CONE_UNR : 1;
         const uint32_t nq = (C - head) / NV;
         for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
             typename Vec16<W>::T buf[UNR][GP];

@@ -82,6 +82,7 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
         void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
                                      : gam == 2 ? k_clg_fwd<F30, CL, 2> : k_clg_fwd<F30, CL, 3>;
         if (set_smem(kg, smem)) return -1;
+        lc.blockDim = dim3(TFTB_CLG_NT, 1, 1);
         CK(cudaLaunchKernelEx(&lc, kg, a));
     } else {
         CK(cudaLaunchKernelEx(&lc, k_cl_inv<F30, CL>, a));

@@ -153,6 +153,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
                 void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
                                            : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
                 if (set_smem(kg, smem)) return -1;
+                lc.blockDim = dim3(TFTB_CLG_NT, 1, 1);
                 CK(cudaLaunchKernelEx(&lc, kg, a));
             }
             g_launches++;

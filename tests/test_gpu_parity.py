@@ -342,4 +342,4 @@ def test_device_footprint_audit():
         T.tft(x, cfg)
         T.itft(x, cfg)
         peaks.append(backend.aux_bytes())
-    assert max(peaks) <= 2 ** 14 * 4 + 4096, peaks
+    assert max(peaks) <= 2 ** 14 * 4 + 32768, peaks  # one chunk stash + p2r partial sums
