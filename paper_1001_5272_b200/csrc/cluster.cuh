@@ -466,11 +466,14 @@ TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg
 // 16-byte alignment, C being a multiple of 4) and 2 quads in flight, so the
 // L2 round trips are 8x fewer than with scalar loads; ragged head and tail
 // columns go through col_solve_range.
+#ifndef TFTB_QIF2_MAXM
+#define TFTB_QIF2_MAXM 3
+#endif
 template <class F, int M>
 TFT_DEV void col2_quads(const F& f, typename F::W* x, const typename F::W* S, uint32_t C, uint32_t h,
                         const Tw<typename F::W>* blk, const typename F::W* blkM) {
     using W = typename F::W;
-    constexpr int K = M - 1, QIF = M <= 3 ? 2 : 1;
+    constexpr int K = M - 1, QIF = M <= TFTB_QIF2_MAXM ? 2 : 1;
     auto ld = [&](int j, uint32_t c) { return (uint32_t)j < (uint32_t)K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
     auto nx = [](uint32_t, W) {};
     const uint32_t mis = (uint32_t)(((uintptr_t)x & 15) / sizeof(W));
@@ -553,7 +556,13 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
     TFTB_STAMP(a, 2);
-    cl.sync();
+    cluster_arrive_release();
+    // a complete chunk's columns < h are final after step 1: publish them for
+    // the last CTA's second solve (read back from L2) while the cluster
+    // barrier settles -- they need only this CTA's own tile
+    if (h && g < K)
+        for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
+    cluster_wait_acquire();
     TFTB_STAMP(a, 3);
 
     W* rs[9];
@@ -569,13 +578,9 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
             [&](uint32_t c, W w) { rs[K][c + (c >> 5)] = w; }, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1),
             a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
     }
-    // a complete chunk's columns < h are final after step 1: publish them for
-    // the last CTA's second solve (read back from L2), then leave -- the last
-    // chunk's solve below needs nobody else's tile
-    if (h && g < K)
-        for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
     TFTB_STAMP(a, 4);
-    // (also the exit barrier: no CTA may leave while others still read its tile)
+    // exit barrier: no CTA may leave while others still read its tile; then
+    // the last chunk's solve below needs nobody else's tile
     cl.sync();
     if (!h || g != K) return;
     TFTB_STAMP(a, 5);

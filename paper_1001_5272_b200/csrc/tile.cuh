@@ -234,12 +234,13 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             const uint32_t B = h - hd, H = 1u << (d - 1);
             if (hd >= H) {
                 const uint32_t cnt = (hd - H) << tl.wlog;
+                const Tw<W> wh = cnt ? f.tw(f.twmul(w, R.inv2)) : w;  // w / 2: one product per element
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
                     uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
                     W lo = f.canon(tl.at(tl.ix(B + i, col)));
                     W hi = tl.at(tl.ix(B + H + i, col));
                     tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.cmulw(f.csub(lo, hi), w), R.inv2);
+                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.csub(lo, hi), wh);
                 }
             } else {
                 const uint32_t cnt = hd << tl.wlog;
