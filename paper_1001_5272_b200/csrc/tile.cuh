@@ -195,11 +195,22 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
         const uint32_t hd = h & ((1u << d) - 1), B = h - hd;
         return hd >= (1u << (d - 1)) ? tpi.get(d - 1, B >> d) : tpf.get(d - 1, B >> d);
     };
-    Tw<W> wn = act && t >= dact ? tw2(t) : Tw<W>{};
-    Tw<W> wn3 = act && dact <= t ? tw3(dact) : Tw<W>{};
+    // one tile per CTA: every level's twiddles are fetched at once into
+    // shared memory (one global-memory latency instead of one per level)
+    __shared__ Tw<W> pre2[16], pre3[16];
+    const bool pre = !uniform && t < 16;
+    if (pre) {
+        for (int d = dact + (int)ln.id; d <= t; d += (int)ln.n) {
+            pre2[d] = tw2(d);
+            pre3[d] = tw3(d);
+        }
+        __syncthreads();
+    }
+    Tw<W> wn = !pre && act && t >= dact ? tw2(t) : Tw<W>{};
+    Tw<W> wn3 = !pre && act && dact <= t ? tw3(dact) : Tw<W>{};
     for (int d = t; d >= dlo; --d) {
-        const Tw<W> w = wn;
-        if (act && d - 1 >= dact) wn = tw2(d - 1);
+        const Tw<W> w = pre ? pre2[d] : wn;
+        if (!pre && act && d - 1 >= dact) wn = tw2(d - 1);
         if (d >= dact) {
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
@@ -227,8 +238,8 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
         __syncthreads();
     }
     for (int d = dlo; d <= t; ++d) {
-        const Tw<W> w = wn3;
-        if (act && d >= dact && d + 1 <= t) wn3 = tw3(d + 1);
+        const Tw<W> w = pre ? pre3[d] : wn3;
+        if (!pre && act && d >= dact && d + 1 <= t) wn3 = tw3(d + 1);
         if (d >= dact) {
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);

@@ -1,46 +1,42 @@
-"""profiles/traffic.json from an ncu launch CSV of `bench.py --steps 1`.
+"""profiles/traffic.json from an ncu launch capture of the config-2 bench.
 
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-        --clock-control none --csv --log-file launches.csv \
+        --clock-control none --csv --log-file traffic.csv \
         python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e
-    python tools/traffic.py launches.csv > profiles/traffic.json
+    python tools/traffic.py traffic.csv > profiles/traffic.json
 
-The timed step is the last `per_step` tftb launches (forward groups, then
-inverse groups).  ncu serialises and cold-starts each launch, so only the
-byte counts and the kernels' shares are meaningful, not the absolute times.
+The last four tftb200 launches are the timed step (two forward size-class
+launches, then two inverse ones); ncu serialises and cold-starts them, so the
+bytes are the evidence here, not the times.
 """
 import csv
 import json
 import sys
 from collections import OrderedDict
 
-rows = [r for r in csv.reader(open(sys.argv[1])) if r]
-per_step = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-h = next(r for r in rows if r[0] == "ID")
-ii, ki, mi, vi = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
-launch = OrderedDict()
-for r in rows[rows.index(h) + 1:]:
-    if len(r) != len(h) or not r[ii].isdigit():
+rows = list(csv.reader(open(sys.argv[1])))
+start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+h = rows[start]
+ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+launches = OrderedDict()
+for r in rows[start + 1:]:
+    if len(r) <= vi:
         continue
-    d = launch.setdefault(int(r[ii]), {"kernel": r[ki].split("(")[0]})
+    d = launches.setdefault(r[ii], {"kernel": r[ki].split("(")[0]})
     d[r[mi]] = float(r[vi].replace(",", ""))
-ours = [d for d in launch.values() if d["kernel"].startswith("void k_")]
-step = ours[-per_step:]
-out = {
-    "source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-              "--clock-control none (cold, serialised) on bench.py --steps 1 --warmup 3; "
-              f"last {per_step} tftb launches = the timed step",
-    "launches": [{"kernel": d["kernel"], "ns": d.get("gpu__time_duration.sum"),
-                  "dram_read": d.get("dram__bytes_read.sum"), "dram_write": d.get("dram__bytes_write.sum")}
-                 for d in step],
-}
-rd = sum(d["dram_read"] for d in out["launches"])
-wr = sum(d["dram_write"] for d in out["launches"])
-out["config2_bytes_per_step"] = rd + wr
-out["config2_read_bytes"] = rd
-out["config2_write_bytes"] = wr
-inv = [d for d in out["launches"] if "inv" in d["kernel"]]
-out["inverse_pass_bytes"] = sum(d["dram_read"] + d["dram_write"] for d in inv)
+ours = [d for d in launches.values() if d["kernel"].split("<")[0].split()[-1] in ("k_clg_fwd", "k_cl_inv")][-4:]
+out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
+                 "--clock-control none (cold, serialised) on bench.py --steps 1 --warmup 3; last 4 tftb "
+                 "launches = the timed step",
+       "launches": [{"kernel": d["kernel"], "ns": d["gpu__time_duration.sum"],
+                     "dram_read": d["dram__bytes_read.sum"], "dram_write": d["dram__bytes_write.sum"]}
+                    for d in ours]}
+tot = lambda ds: sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds)
+inv = [d for d in ours if "k_cl_inv" in d["kernel"]]
+out["config2_bytes_per_step"] = tot(ours)
+out["config2_read_bytes"] = sum(d["dram__bytes_read.sum"] for d in ours)
+out["config2_write_bytes"] = sum(d["dram__bytes_write.sum"] for d in ours)
+out["inverse_pass_bytes"] = tot(inv)
 out["inverse_pass_kernel"] = inv[0]["kernel"] if inv else None
-out["config2_ncu_step_ns"] = sum(d["ns"] for d in out["launches"])
+out["config2_ncu_step_ns"] = sum(d["gpu__time_duration.sum"] for d in ours)
 print(json.dumps(out, indent=1))
