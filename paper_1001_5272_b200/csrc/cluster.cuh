@@ -44,6 +44,28 @@ namespace cg = cooperative_groups;
 // split cluster barrier (every thread of the CTA arrives / waits)
 TFT_DEV void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 TFT_DEV void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+TFT_DEV void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+
+// mbarrier signalling between the CTAs of a cluster (one phase, parity 0)
+TFT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+TFT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arrive (release, cluster scope) on the same mbarrier in CTA `rank`
+TFT_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+TFT_DEV void mbar_wait_cluster(uint64_t* bar) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], 0; selp.u32 %0, 1, 0, P; }"
+            : "=r"(done) : "r"(a) : "memory");
+}
 
 // read-only load of one twiddle pair
 template <typename W>
@@ -272,8 +294,16 @@ TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const T
         } else {
             reg_inv<F, KK, 0, false>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
         }
+        if constexpr (MASK) {
+            // only rows < h change; the rest is not written back, so another
+            // CTA may fill the tail [h, 2^TL) concurrently (k_cl_inv step 2)
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
+            for (int i = 0; i < (1 << KK); ++i)
+                if (base + ((uint32_t)i << SLO) < h) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
+        } else {
+#pragma unroll
+            for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
+        }
     }
 }
 
@@ -531,6 +561,7 @@ template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
 __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t rows_ready;  // complete CTAs: every step-1 row is in DSMEM
     W* S = reinterpret_cast<W*>(smem_raw);
     cg::cluster_group cl = cg::this_cluster();
     const uint32_t g = cl.block_rank(), G = cl.num_blocks();
@@ -538,51 +569,66 @@ __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     const int64_t v = a.vbase + blockIdx.y;
     const int64_t n = a.xd.n(v);
     const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    const bool last = h && g == K;  // the partial chunk (G = K + 1 when h != 0)
     const int64_t o = a.xd.o(v);
     W* x = a.x + o;
     const F f = a.f;
     const int64_t cbase = (int64_t)g * C;
     TFTB_STAMP(a, 0);
+    // Step 2 needs the K complete chunks' step-1 rows, and writes into the
+    // last chunk's tail [h, C) (which that CTA's loads must have zeroed
+    // first) -- it does not need the last chunk's own, slower, masked phase 1.
+    // So instead of a cluster-wide barrier, each complete CTA counts K + 1
+    // remote arrivals on an mbarrier: one per complete CTA after step 1, one
+    // from the last CTA after its load.
+    if (threadIdx.x == 0) mbar_init(&rows_ready, K + (h ? 1 : 0));
+    cluster_arrive_relaxed();  // (inits visible before any remote arrive)
     if (a.pre)
         tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
     else
         tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
     TFTB_STAMP(a, 1);
-    // step 1, and phase 1 of the last chunk's solve (it reads only that chunk's
-    // known outputs [0, h), never the tail the columns will fill) alongside
-    const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
-    // complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
-    if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
-    else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
-    TFTB_STAMP(a, 2);
-    cluster_arrive_release();
-    // a complete chunk's columns < h are final after step 1: publish them for
-    // the last CTA's second solve (read back from L2) while the cluster
-    // barrier settles -- they need only this CTA's own tile
-    if (h && g < K)
-        for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
     cluster_wait_acquire();
-    TFTB_STAMP(a, 3);
-
-    W* rs[9];
+    const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
+    if (last) {
+        if (threadIdx.x == 0)
+            for (uint32_t j = 0; j < K; ++j) mbar_arrive_remote(&rows_ready, j);
+        // phase 1 of the last chunk's solve: it touches only [0, h)
+        inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+        TFTB_STAMP(a, 2);
+        TFTB_STAMP(a, 3);
+        TFTB_STAMP(a, 4);
+    } else {
+        // step 1: complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
+        inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
+        TFTB_STAMP(a, 2);
+        if (threadIdx.x == 0)
+            for (uint32_t j = 0; j < K; ++j) mbar_arrive_remote(&rows_ready, j);
+        // columns < h are final after step 1: publish them for the last
+        // CTA's second solve (read back from L2) while the siblings finish
+        if (h)
+            for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
+        mbar_wait_cluster(&rows_ready);
+        TFTB_STAMP(a, 3);
+        W* rs[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
-    {
-        // columns >= h: K known rows; their coefficients are final, the next
-        // output of each goes into the last chunk's tile
+        for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
+        // step 2, columns >= h, shared by the K complete CTAs: K known rows;
+        // their coefficients are final, the next output of each goes into
+        // the last chunk's tail
         uint32_t lo, hi;
-        col_share(h, C, g, G, lo, hi);
+        col_share(h, C, g, K, lo, hi);
         col_solve(
             f, [&](int j, uint32_t c) { return rs[j][c + (c >> 5)]; },
             [&](uint32_t c, W w) { rs[K][c + (c >> 5)] = w; }, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1),
             a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
+        TFTB_STAMP(a, 4);
     }
-    TFTB_STAMP(a, 4);
-    // exit barrier: no CTA may leave while others still read its tile; then
-    // the last chunk's solve below needs nobody else's tile
+    // exit barrier: no CTA may leave while others still read its tile, and
+    // the last chunk's solve needs every column's next output
     cl.sync();
-    if (!h || g != K) return;
+    if (!last) return;
     TFTB_STAMP(a, 5);
     {
         SmemTile<W> tl{S, CL, 0};
