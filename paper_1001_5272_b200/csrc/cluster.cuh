@@ -912,6 +912,108 @@ TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, cons
     return vals[0];
 }
 
+// Row g of the cone (compile-time g: the half selections are constants),
+// canonical inputs (see cone_row).
+template <class F, int GAM, int GI>
+TFT_DEV typename F::W cone_row_ct(const F& f, typename F::W* vals, const Tw<typename F::W>* tw) {
+    using W = typename F::W;
+    if constexpr (!F::kLazy) {
+        return cone_row<F, GAM>(f, vals, GI, tw);
+    } else {
+        constexpr int GP = 1 << GAM;
+        {
+            constexpr int H = GP / 2;
+            constexpr bool sel = (GI >> (GAM - 1)) & 1;
+#pragma unroll
+            for (int i = 0; i < H; ++i) vals[i] = sel ? vals[i] - vals[i + H] + f.p : vals[i] + vals[i + H];
+        }
+#pragma unroll
+        for (int sp = GAM - 2; sp >= 0; --sp) {
+            const int H = 1 << sp;
+            const bool sel = (GI >> sp) & 1;
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                const W a = sp == GAM - 2 ? vals[i] : f.red2(vals[i]);
+                const W b = f.mulw(vals[i + H], tw[sp]);
+                vals[i] = sel ? a - b + f.p2 : a + b;
+            }
+        }
+        return vals[0];
+    }
+}
+
+// S[i] <- row GI of column i's cone, i < 2^CL, reading the GP rows
+// in[j 2^CL + i] (positions >= nin are zeros).  Rows share their 16-byte
+// alignment: scalar head, then quads -- per row a quad is full, empty or
+// (at most once per row) partial, decided on 32-bit offsets against the
+// row's precomputed length -- then a scalar tail.
+template <class F, int CL, int GAM, int GI>
+TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, int64_t nin,
+                       const Tw<typename F::W>* Zf) {
+    using W = typename F::W;
+    using V = Vec16<W>;
+    constexpr uint32_t C = 1u << CL;
+    constexpr int GP = 1 << GAM, NV = V::N;
+    Tw<W> tw[GAM > 1 ? GAM - 1 : 1];
+#pragma unroll
+    for (int sp = 0; sp < GAM - 1; ++sp) tw[sp] = Zf[GI >> (sp + 1)];
+    const uint32_t mis = (uint32_t)(((uintptr_t)in & 15) / sizeof(W));
+    const uint32_t head = (NV - mis) % NV;
+    uint32_t len[GP];  // words of row j present from position head on
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+        const int64_t r = nin - (int64_t)j * C - head;
+        len[j] = r <= 0 ? 0u : (uint32_t)min(r, (int64_t)C);
+    }
+    auto one = [&](uint32_t i) {
+        W vals[GP];
+#pragma unroll
+        for (int j = 0; j < GP; ++j) vals[j] = (int64_t)j * C + i < nin ? in[(size_t)j * C + i] : W(0);
+        S[i + (i >> 5)] = cone_row_ct<F, GAM, GI>(f, vals, tw);
+    };
+    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
+    const uint32_t nq = (C - head) / NV;
+    const W* base = in + head;
+    constexpr int UNR = GP <= 4 ? TFTB_CONE_UNR : 1;
+    for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
+        typename V::T buf[UNR][GP];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t o = (q0 + u * blockDim.x) * NV;
+#pragma unroll
+            for (int j = 0; j < GP; ++j) {
+                const W* src = base + (size_t)j * C + o;
+                if (o + NV <= len[j]) {
+                    // the vector's other CTAs read the same rows: keep them in L2
+                    buf[u][j] = __ldcg(reinterpret_cast<const typename V::T*>(src));
+                } else if (o >= len[j]) {
+                    buf[u][j] = V::zero();
+                } else {
+                    W e[NV];
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) e[k] = o + k < len[j] ? src[k] : W(0);
+                    buf[u][j] = V::make(e);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t q = q0 + u * blockDim.x;
+            if (q >= nq) break;
+            const uint32_t i0 = head + q * NV;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                W vals[GP];
+#pragma unroll
+                for (int j = 0; j < GP; ++j) vals[j] = V::get(buf[u][j], k);
+                const uint32_t i = i0 + k;
+                S[i + (i >> 5)] = cone_row_ct<F, GAM, GI>(f, vals, tw);
+            }
+        }
+    }
+    for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
+}
+
 #ifndef TFTB_CLG_NT
 #define TFTB_CLG_NT 256
 #endif
@@ -939,62 +1041,15 @@ __global__ void __launch_bounds__(TFTB_CLG_NT, TFTB_CLG_MINB) k_clg_fwd(LaunchAr
     W* x = a.x + a.xd.o(v);
     const W* in = a.in + a.ind.o(v);
     TFTB_STAMP(a, 0);
-    Tw<W> tw[GAM > 1 ? GAM - 1 : 1];
-#pragma unroll
-    for (int sp = 0; sp < GAM - 1; ++sp) tw[sp] = a.R.Zf[g >> (sp + 1)];
-    // rows j*C + i share their alignment (C is a multiple of the vector):
-    // scalar head up to 16-byte alignment, quads, scalar tail
-    const uint32_t mis = (uint32_t)(((uintptr_t)in & 15) / sizeof(W));
-    const uint32_t head = (NV - mis) % NV;
-    auto one = [&](uint32_t i) {
-        W vals[GP];
-#pragma unroll
-        for (int j = 0; j < GP; ++j) {
-            const int64_t pos = (int64_t)j * C + i;
-            vals[j] = pos < nin ? in[pos] : W(0);
-        }
-        S[i + (i >> 5)] = cone_row<F, GAM>(f, vals, g, tw);
-    };
-    for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
-    {
-        constexpr int UNR = GP <= 4 ? TFTB_CONE_UNR : 1;
-        const uint32_t nq = (C - head) / NV;
-        for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
-            typename Vec16<W>::T buf[UNR][GP];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t q = q0 + u * blockDim.x;
-#pragma unroll
-                for (int j = 0; j < GP; ++j) {
-                    const int64_t pos = (int64_t)j * C + head + (int64_t)q * NV;
-                    if (q < nq && pos + NV <= nin) {
-                        // the vector's other CTAs read the same rows: keep them in L2
-                        buf[u][j] = __ldcg(reinterpret_cast<const typename Vec16<W>::T*>(in + pos));
-                    } else if (pos >= nin) {
-                        buf[u][j] = Vec16<W>::zero();
-                    } else {
-                        W e[NV];
-#pragma unroll
-                        for (int k = 0; k < NV; ++k) e[k] = (q < nq && pos + k < nin) ? in[pos + k] : W(0);
-                        buf[u][j] = Vec16<W>::make(e);
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t q = q0 + u * blockDim.x;
-                if (q >= nq) break;
-#pragma unroll
-                for (int k = 0; k < NV; ++k) {
-                    W vals[GP];
-#pragma unroll
-                    for (int j = 0; j < GP; ++j) vals[j] = Vec16<W>::get(buf[u][j], k);
-                    const uint32_t i = head + q * NV + k;
-                    S[i + (i >> 5)] = cone_row<F, GAM>(f, vals, g, tw);
-                }
-            }
-        }
-        for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
+    switch (g) {  // the cone's half selections are compile-time per CTA
+        case 0: cone_fill<F, CL, GAM, 0>(f, S, in, nin, a.R.Zf); break;
+        case 1: cone_fill<F, CL, GAM, 1>(f, S, in, nin, a.R.Zf); break;
+        case 2: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 2>(f, S, in, nin, a.R.Zf); break;
+        case 3: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 3>(f, S, in, nin, a.R.Zf); break;
+        case 4: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 4>(f, S, in, nin, a.R.Zf); break;
+        case 5: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 5>(f, S, in, nin, a.R.Zf); break;
+        case 6: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 6>(f, S, in, nin, a.R.Zf); break;
+        default: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 7>(f, S, in, nin, a.R.Zf); break;
     }
     TFTB_STAMP(a, 1);
     // In place (in == x), chunk g is also a row of every sibling CTA's
