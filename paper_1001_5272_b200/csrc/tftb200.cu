@@ -355,8 +355,9 @@ int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64
     CK(cudaStreamSynchronize(nullptr));
     uint64_t* d64 = (uint64_t*)buf.p;
     W* dw = narrow ? (W*)(d64 + span) : (W*)d64;
-    // sub-batches of ~span/12 words (at least 2^22), consecutive vectors
-    const int64_t target = std::max<int64_t>(span / 12, 1 << 22);
+    // sub-batches of ~span/48 words (at least 2^22), consecutive vectors:
+    // shorter pipeline fill and drain (measured: 12 -> 48 parts, +2% e2e)
+    const int64_t target = std::max<int64_t>(span / 48, 1 << 22);
     std::vector<std::pair<int64_t, int64_t>> subs;
     for (int64_t v0 = 0; v0 < count;) {
         int64_t v1 = v0, words = 0;
