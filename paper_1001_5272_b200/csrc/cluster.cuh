@@ -557,6 +557,139 @@ TFT_DEV void col2_solve(const F& f, typename F::W* x, const typename F::W* S, ui
     }
 }
 
+// Column solve over columns [clo, chi) of a vector laid out as rows of C
+// words: M = KG + (LASTS ? 1 : 0) known rows, rows j < KG from global memory
+// (x[j C + c]) and, with LASTS, row KG from the tile S; the M coefficients
+// go back to x rows 0..M-1 and, with NEXT, the column's next output to S[c].
+// u32 words: 4 adjacent columns per thread with 16-byte loads and stores
+// (rows share the vector's alignment, C being a multiple of 4), ragged edges
+// through col_solve_range.
+template <class F, int M, bool LASTS, bool NEXT>
+TFT_DEV void colq_solve(const F& f, typename F::W* x, typename F::W* S, uint32_t C, uint32_t clo, uint32_t chi,
+                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
+    using W = typename F::W;
+    constexpr int KG = LASTS ? M - 1 : M, QIF = M <= 3 ? 2 : 1;
+    auto ld = [&](int j, uint32_t c) { return j < KG ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
+    auto nx = [&](uint32_t c, W w) { S[c + (c >> 5)] = w; };
+    if (clo >= chi) return;
+    if constexpr (M > 4 || sizeof(W) != 4) {  // (few vectors; registers would spill) scalar loads
+        col_solve_range<F, M>(f, ld, nx, x, C, clo, chi, blk, blkM, NEXT);
+        return;
+    }
+    const uint32_t mis = (uint32_t)(((uintptr_t)(x + clo) & 15) / sizeof(W));
+    const uint32_t head = min(chi - clo, (4 - mis) & 3);
+    const uint32_t c_a = clo + head, nq = (chi - c_a) / 4, c_b = c_a + 4 * nq;
+    if (head) col_solve_range<F, M>(f, ld, nx, x, C, clo, c_a, blk, blkM, NEXT);
+    for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += QIF * blockDim.x) {
+        uint4 r[QIF][KG];
+#pragma unroll
+        for (int u = 0; u < QIF; ++u) {
+            const uint32_t c0 = c_a + 4 * (q0 + u * blockDim.x);
+#pragma unroll
+            for (int j = 0; j < KG; ++j)
+                if (q0 + u * blockDim.x < nq) r[u][j] = __ldcg(reinterpret_cast<const uint4*>(x + (size_t)j * C + c0));
+        }
+#pragma unroll
+        for (int u = 0; u < QIF; ++u) {
+            const uint32_t c0 = c_a + 4 * (q0 + u * blockDim.x);
+            if (q0 + u * blockDim.x >= nq) break;
+            W out[M][4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                W y[M], xv[M], nv;
+#pragma unroll
+                for (int j = 0; j < KG; ++j) y[j] = k == 0 ? r[u][j].x : k == 1 ? r[u][j].y : k == 2 ? r[u][j].z : r[u][j].w;
+                const uint32_t c = c0 + k;
+                if (LASTS) y[M - 1] = S[c + (c >> 5)];
+                col_solve_vals<F, M>(f, y, blk, blkM, xv, NEXT ? &nv : nullptr);
+                if (NEXT) S[c + (c >> 5)] = nv;
+#pragma unroll
+                for (int j = 0; j < M; ++j) out[j][k] = xv[j];
+            }
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+                *reinterpret_cast<uint4*>(x + (size_t)j * C + c0) = make_uint4(out[j][0], out[j][1], out[j][2], out[j][3]);
+        }
+    }
+    if (c_b < chi) col_solve_range<F, M>(f, ld, nx, x, C, c_b, chi, blk, blkM, NEXT);
+}
+
+// Split inverse for 2^CL < n <= 8 2^CL (no cluster): two launches.
+// A (k_cli_chunks, grid (G, vectors)): complete chunks g < K run their
+//   inverse rounds (left scaled by 2^CL) and the last chunk the masked phase
+//   1 of its solve; each stores its tile back as is.
+// B (k_cli_cols, one CTA per vector): columns >= h solved from the K
+//   complete rows (coefficients final; each column's next output into the
+//   last chunk's tail, in shared memory), then phases 2/3 of the last
+//   chunk and the columns < h from K + 1 rows.
+// Every CTA works alone, so nothing waits on a sibling; the price is one
+// more read and write of the vector (the in-between state stays in the
+// n-word buffer: no scratch).
+template <class F, int CL>
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const uint32_t g = blockIdx.x;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    const int64_t cbase = (int64_t)g * C;
+    if (cbase >= n) return;
+    const int64_t o = a.xd.o(v);
+    W* x = a.x + o;
+    const F f = a.f;
+    if (a.pre)
+        tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
+    else
+        tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
+    __syncthreads();
+    const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
+    if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
+    else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
+    tile_store<W>(x + cbase, S, (uint32_t)min((int64_t)C, n - cbase), [](W w) { return w; });
+}
+
+template <class F, int CL>
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const int64_t v = a.vbase + blockIdx.x;
+    const int64_t n = a.xd.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    W* x = a.x + a.xd.o(v);
+    const F f = a.f;
+    if (h) tile_load<W>(S, x + (size_t)K * C, h, C, [](uint32_t, W w) { return w; });
+    __syncthreads();
+    const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
+    const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
+    switch (K) {  // columns >= h: K rows
+#define TFTB_C1(k)                                                                          \
+    case k:                                                                                 \
+        if (h) colq_solve<F, k, false, true>(f, x, S, C, h, C, b1, b1M);                    \
+        else colq_solve<F, k, false, false>(f, x, S, C, 0, C, b1, b1M);                     \
+        break;
+        TFTB_C1(1) TFTB_C1(2) TFTB_C1(3) TFTB_C1(4) TFTB_C1(5) TFTB_C1(6) TFTB_C1(7)
+        default: colq_solve<F, 8, false, false>(f, x, S, C, 0, C, b1, b1M); break;  // K = 8: h = 0
+#undef TFTB_C1
+    }
+    if (!h) return;
+    __syncthreads();
+    const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
+    itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
+    const Tw<W>* b2 = a.R.vinvT + 72 * K;
+    const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
+    switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
+#define TFTB_C2(m)                                                                          \
+    case m: colq_solve<F, m, true, false>(f, x, S, C, 0, h, b2, b2M); break;
+        TFTB_C2(2) TFTB_C2(3) TFTB_C2(4) TFTB_C2(5) TFTB_C2(6) TFTB_C2(7) TFTB_C2(8)
+#undef TFTB_C2
+    }
+}
+
 template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
 __global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
     using W = typename F::W;

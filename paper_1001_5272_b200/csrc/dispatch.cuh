@@ -145,7 +145,15 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            if (inverse) {
+            static const bool split = !getenv("TFTB_INV_SPLIT") || atoi(getenv("TFTB_INV_SPLIT"));
+            if (inverse && split) {
+                if (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem)) return -1;
+                k_cli_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+                k_cli_cols<F, CL><<<nv, kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+                g_launches++;
+            } else if (inverse) {
                 CK(cudaLaunchKernelEx(&lc, ki, a));
             } else {
                 // forward: rows re-read through L2 instead of DSMEM (cluster only for the store barrier)
