@@ -6,6 +6,22 @@
 
 namespace tftb {
 
+// side streams for concurrent plan groups (per device, created once)
+constexpr int kGroupStreams = 4;
+inline cudaStream_t* group_streams() {
+    static std::mutex mu;
+    static std::map<int, std::vector<cudaStream_t>> per_dev;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto& v = per_dev[dev];
+    if (v.empty()) {
+        v.resize(kGroupStreams);
+        for (auto& s : v) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    }
+    return v.data();
+}
+
 // whole-vector tiles of one size class T = ceil_lg(n)
 template <class F, int T>
 int launch_tiles(LaunchArgs<F> a, int64_t count, bool inverse, cudaStream_t st) {
@@ -349,14 +365,49 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
 template <class F>
 int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st) {
     using W = typename F::W;
+    // Groups are independent vectors.  Tile and cluster groups (no shared
+    // stash, no scratch) fork onto side streams so one launch's tail wave
+    // overlaps the next one's start; the join keeps `st` ordered after all
+    // (graph-capture safe: fork/join through events).
+    static const bool fork_ok = !getenv("TFTB_GROUP_STREAMS") || atoi(getenv("TFTB_GROUP_STREAMS"));
+    bool fork = fork_ok && P->groups.size() > 1;
     for (const auto& g : P->groups) {
+        Plan pl;
+        if (make_plan<F>(g.maxn, &pl)) return -1;
+        fork &= pl.kind == kSmall || pl.kind == kCluster;
+    }
+    cudaStream_t* side = fork ? group_streams() : nullptr;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
+    if (fork) {
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_fork, st));
+    }
+    int rc = 0;
+    for (size_t i = 0; i < P->groups.size() && !rc; ++i) {
+        const auto& g = P->groups[i];
         const int64_t* d = (const int64_t*)P->darr + g.arr_off;
         VecDesc<W> xd{d, d + g.count, 0, 0};
-        if (run_group<F>(P->rh, (W*)data, nullptr, (const W*)pre, g.count, xd, xd, g.maxn, inverse != 0, st,
-                         (W*)P->stash))
-            return -1;
+        cudaStream_t gs = st;
+        if (fork) {
+            gs = side[i % kGroupStreams];
+            CK(cudaStreamWaitEvent(gs, ev_fork, 0));
+        }
+        rc = run_group<F>(P->rh, (W*)data, nullptr, (const W*)pre, g.count, xd, xd, g.maxn, inverse != 0, gs,
+                          (W*)P->stash);
+        if (fork) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, gs));
+            ev_join.push_back(e);
+        }
     }
-    return 0;
+    for (auto e : ev_join) {
+        CK(cudaStreamWaitEvent(st, e, 0));
+        cudaEventDestroy(e);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    return rc;
 }
 
 // Partition a batch by plan (ceil_lg of the length class) and run each group.
