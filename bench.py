@@ -327,7 +327,7 @@ def main():
 
     if rank == 0:
         peak, peak_kind = peaks()
-        # dominant kernel: the inverse pass (k_cl_inv, both size-class launches),
+        # dominant kernel: the inverse pass (k_cli_chunks + k_cli_cols, both size classes),
         # its algorithmic bytes over its own event-timed duration, per GPU
         achieved = alg_bytes_all / (inv_ms_max / 1e3) / 1e9 / world
         step_achieved = 2 * alg_bytes_all / (step_ms_max / 1e3) / 1e9 / world
@@ -355,7 +355,7 @@ def main():
             "roundtrip_exact": ok_all,
             "gpu_launches": launches,
             "clocks": clk,
-            "roofline": {"bound": "hbm", "kernel": "k_cl_inv (inverse pass)", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "inverse pass (k_cli_chunks + k_cli_cols)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": None,
                          "step_achieved": step_achieved, "step_frac": step_achieved / peak,

@@ -11,13 +11,13 @@
 // the network: twiddles omega_{2J} at global J).  A split cluster barrier
 // keeps every chunk store behind all siblings' row reads (in place).
 //
-// Inverse (k_cl_inv, one G-CTA cluster per vector; K = n >> CL complete
-// chunks, h = n mod 2^CL):
+// Inverse (K = n >> CL complete chunks, h = n mod 2^CL), split in two
+// launches, k_cli_chunks then k_cli_cols:
 //   1. chunks g < K: inverse of the CL local stages (left scaled by 2^CL);
 //      chunk K: phase 1 of its masked inverse;
-//   2. columns c >= h (over DSMEM): K known outputs -> K coefficients by
-//      V_K^-1 (REDC dot products; results straight to HBM), and the column's
-//      next output sum_j x_j omega_K^j into chunk K's slot c;
+//   2. columns c >= h: K known outputs -> K coefficients by V_K^-1 (REDC
+//      dot products; results straight to the vector), and the column's next
+//      output sum_j x_j omega_K^j into chunk K's slot c (shared memory);
 //   3. chunk K: generalised in-tile inverse with h known outputs and the
 //      2^CL - h values from step 2 as its known tail;
 //   4. columns c < h: K+1 known outputs -> coefficients by V_{K+1}^-1.
@@ -27,9 +27,6 @@
 #pragma once
 #include <cooperative_groups.h>
 
-#ifndef TFTB_MINB32
-#define TFTB_MINB32 3
-#endif
 
 #include "kernels.cuh"
 #include <type_traits>
@@ -37,35 +34,13 @@
 // CTAs per SM the 256-thread tile kernels are compiled for: 3 (80 registers)
 // for u32 words; u64 words need twice the registers per 32-word unit, so 2
 template <class F>
-constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : TFTB_MINB32; }
+constexpr int kern_minb() { return sizeof(typename F::W) == 8 ? 2 : 3; }
 
 namespace cg = cooperative_groups;
 
 // split cluster barrier (every thread of the CTA arrives / waits)
 TFT_DEV void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 TFT_DEV void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-TFT_DEV void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
-
-// mbarrier signalling between the CTAs of a cluster (one phase, parity 0)
-TFT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-TFT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// arrive (release, cluster scope) on the same mbarrier in CTA `rank`
-TFT_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
-    uint32_t remote;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
-TFT_DEV void mbar_wait_cluster(uint64_t* bar) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    while (!done)
-        asm volatile(
-            "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], 0; selp.u32 %0, 1, 0, P; }"
-            : "=r"(done) : "r"(a) : "memory");
-}
 
 // read-only load of one twiddle pair
 template <typename W>
@@ -296,7 +271,7 @@ TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const T
         }
         if constexpr (MASK) {
             // only rows < h change; the rest is not written back, so another
-            // CTA may fill the tail [h, 2^TL) concurrently (k_cl_inv step 2)
+            // CTA may fill the tail [h, 2^TL) concurrently (k_cli_cols' column solve)
 #pragma unroll
             for (int i = 0; i < (1 << KK); ++i)
                 if (base + ((uint32_t)i << SLO) < h) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
@@ -489,74 +464,6 @@ TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg
     }
 }
 
-// The last chunk's second column solve, columns [0, h) with M = K + 1 rows:
-// rows j < K come from global memory (L2: the complete chunks published
-// them), row K from this CTA's tile.  u32 words: 4 adjacent columns per
-// thread with 16-byte loads and stores (every row shares the vector's
-// 16-byte alignment, C being a multiple of 4) and 2 quads in flight, so the
-// L2 round trips are 8x fewer than with scalar loads; ragged head and tail
-// columns go through col_solve_range.
-#ifndef TFTB_QIF2_MAXM
-#define TFTB_QIF2_MAXM 3
-#endif
-template <class F, int M>
-TFT_DEV void col2_quads(const F& f, typename F::W* x, const typename F::W* S, uint32_t C, uint32_t h,
-                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
-    using W = typename F::W;
-    constexpr int K = M - 1, QIF = M <= TFTB_QIF2_MAXM ? 2 : 1;
-    auto ld = [&](int j, uint32_t c) { return (uint32_t)j < (uint32_t)K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
-    auto nx = [](uint32_t, W) {};
-    const uint32_t mis = (uint32_t)(((uintptr_t)x & 15) / sizeof(W));
-    const uint32_t head = min(h, (4 - mis) & 3);
-    const uint32_t nq = (h - head) / 4, body_end = head + 4 * nq;
-    if (head) col_solve_range<F, M>(f, ld, nx, x, C, 0, head, blk, blkM, false);
-    for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += QIF * blockDim.x) {
-        uint4 r[QIF][K];
-#pragma unroll
-        for (int u = 0; u < QIF; ++u) {
-            const uint32_t c0 = head + 4 * (q0 + u * blockDim.x);
-#pragma unroll
-            for (int j = 0; j < K; ++j)
-                if (q0 + u * blockDim.x < nq) r[u][j] = __ldcg(reinterpret_cast<const uint4*>(x + (size_t)j * C + c0));
-        }
-#pragma unroll
-        for (int u = 0; u < QIF; ++u) {
-            const uint32_t c0 = head + 4 * (q0 + u * blockDim.x);
-            if (q0 + u * blockDim.x >= nq) break;
-            W out[M][4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                W y[M], xv[M];
-#pragma unroll
-                for (int j = 0; j < K; ++j) y[j] = k == 0 ? r[u][j].x : k == 1 ? r[u][j].y : k == 2 ? r[u][j].z : r[u][j].w;
-                const uint32_t c = c0 + k;
-                y[K] = S[c + (c >> 5)];
-                col_solve_vals<F, M>(f, y, blk, blkM, xv, nullptr);
-#pragma unroll
-                for (int j = 0; j < M; ++j) out[j][k] = xv[j];
-            }
-#pragma unroll
-            for (int j = 0; j < M; ++j)
-                *reinterpret_cast<uint4*>(x + (size_t)j * C + c0) = make_uint4(out[j][0], out[j][1], out[j][2], out[j][3]);
-        }
-    }
-    if (body_end < h) col_solve_range<F, M>(f, ld, nx, x, C, body_end, h, blk, blkM, false);
-}
-
-template <class F>
-TFT_DEV void col2_solve(const F& f, typename F::W* x, const typename F::W* S, uint32_t C, uint32_t h, int m,
-                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
-    switch (m) {
-        case 2: col2_quads<F, 2>(f, x, S, C, h, blk, blkM); break;
-        case 3: col2_quads<F, 3>(f, x, S, C, h, blk, blkM); break;
-        case 4: col2_quads<F, 4>(f, x, S, C, h, blk, blkM); break;
-        default: {  // (G > 4: few vectors; registers would spill) scalar loads
-            auto ld = [&](int j, uint32_t c) { return (uint32_t)j < (uint32_t)(m - 1) ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
-            col_solve(f, ld, [](uint32_t, typename F::W) {}, x, C, 0, h, m, blk, blkM, false);
-        }
-    }
-}
-
 // Column solve over columns [clo, chi) of a vector laid out as rows of C
 // words: M = KG + (LASTS ? 1 : 0) known rows, rows j < KG from global memory
 // (x[j C + c]) and, with LASTS, row KG from the tile S; the M coefficients
@@ -688,96 +595,6 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> 
         TFTB_C2(2) TFTB_C2(3) TFTB_C2(4) TFTB_C2(5) TFTB_C2(6) TFTB_C2(7) TFTB_C2(8)
 #undef TFTB_C2
     }
-}
-
-template <class F, int CL, int MINB = kern_minb<F>(), int NT = 256>
-__global__ void __launch_bounds__(NT, MINB) k_cl_inv(LaunchArgs<F> a) {
-    using W = typename F::W;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint64_t rows_ready;  // complete CTAs: every step-1 row is in DSMEM
-    W* S = reinterpret_cast<W*>(smem_raw);
-    cg::cluster_group cl = cg::this_cluster();
-    const uint32_t g = cl.block_rank(), G = cl.num_blocks();
-    constexpr uint32_t C = 1u << CL;
-    const int64_t v = a.vbase + blockIdx.y;
-    const int64_t n = a.xd.n(v);
-    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
-    const bool last = h && g == K;  // the partial chunk (G = K + 1 when h != 0)
-    const int64_t o = a.xd.o(v);
-    W* x = a.x + o;
-    const F f = a.f;
-    const int64_t cbase = (int64_t)g * C;
-    TFTB_STAMP(a, 0);
-    // Step 2 needs the K complete chunks' step-1 rows, and writes into the
-    // last chunk's tail [h, C) (which that CTA's loads must have zeroed
-    // first) -- it does not need the last chunk's own, slower, masked phase 1.
-    // So instead of a cluster-wide barrier, each complete CTA counts K + 1
-    // remote arrivals on an mbarrier: one per complete CTA after step 1, one
-    // from the last CTA after its load.
-    if (threadIdx.x == 0) mbar_init(&rows_ready, K + (h ? 1 : 0));
-    cluster_arrive_relaxed();  // (inits visible before any remote arrive)
-    if (a.pre)
-        tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
-    else
-        tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
-    __syncthreads();
-    TFTB_STAMP(a, 1);
-    cluster_wait_acquire();
-    const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
-    if (last) {
-        if (threadIdx.x == 0)
-            for (uint32_t j = 0; j < K; ++j) mbar_arrive_remote(&rows_ready, j);
-        // phase 1 of the last chunk's solve: it touches only [0, h)
-        inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
-        TFTB_STAMP(a, 2);
-        TFTB_STAMP(a, 3);
-        TFTB_STAMP(a, 4);
-    } else {
-        // step 1: complete chunks are left scaled by 2^CL; the column matrices carry 2^-CL
-        inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
-        TFTB_STAMP(a, 2);
-        if (threadIdx.x == 0)
-            for (uint32_t j = 0; j < K; ++j) mbar_arrive_remote(&rows_ready, j);
-        // columns < h are final after step 1: publish them for the last
-        // CTA's second solve (read back from L2) while the siblings finish
-        if (h)
-            for (uint32_t c = threadIdx.x; c < h; c += blockDim.x) x[cbase + c] = S[c + (c >> 5)];
-        mbar_wait_cluster(&rows_ready);
-        TFTB_STAMP(a, 3);
-        W* rs[9];
-#pragma unroll
-        for (int j = 0; j < 9; ++j) rs[j] = cl.map_shared_rank(S, j < (int)G ? j : 0);
-        // step 2, columns >= h, shared by the K complete CTAs: K known rows;
-        // their coefficients are final, the next output of each goes into
-        // the last chunk's tail
-        uint32_t lo, hi;
-        col_share(h, C, g, K, lo, hi);
-        col_solve(
-            f, [&](int j, uint32_t c) { return rs[j][c + (c >> 5)]; },
-            [&](uint32_t c, W w) { rs[K][c + (c >> 5)] = w; }, x, C, lo, hi, (int)K, a.R.vinvS + 72 * (K - 1),
-            a.R.vinvM + 8 * 72 + 72 * (K - 1), h != 0);
-        TFTB_STAMP(a, 4);
-    }
-    // exit barrier: no CTA may leave while others still read its tile, and
-    // the last chunk's solve needs every column's next output
-    cl.sync();
-    if (!last) return;
-    TFTB_STAMP(a, 5);
-    {
-        SmemTile<W> tl{S, CL, 0};
-        itft_phases23(f, tl, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
-    }
-    TFTB_STAMP(a, 6);
-    // columns < h: K + 1 rows, K of them from the complete chunks
-#ifndef TFTB_COL2_SCALAR
-    if constexpr (sizeof(W) == 4)
-        col2_solve(f, x, S, C, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K);
-    else
-#endif
-        col_solve(
-            f, [&](int j, uint32_t c) { return (uint32_t)j < K ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; },
-            [](uint32_t, W) {}, x, C, 0, h, (int)K + 1, a.R.vinvT + 72 * K, a.R.vinvM + 16 * 72 + 72 * K, false);
-    TFTB_STAMP(a, 7);
 }
 
 // ================================================ two-pass plan, chunk pass
@@ -1001,7 +818,6 @@ template <class F, int GAM>
 TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, const Tw<typename F::W>* tw) {
     using W = typename F::W;
     constexpr int GP = 1 << GAM;
-#ifndef TFTB_CONE_GENERIC
     if constexpr (F::kLazy) {
         // inputs are canonical residues: the top stage (theta = 1) gives
         // [0, 2p) without a reduction, so does the second stage's left
@@ -1026,7 +842,6 @@ TFT_DEV typename F::W cone_row(const F& f, typename F::W* vals, uint32_t g, cons
         }
         return vals[0];
     }
-#endif
     // top stage: theta = 1
     {
         constexpr int H = GP / 2;
@@ -1107,7 +922,7 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
     for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
     const uint32_t nq = (C - head) / NV;
     const W* base = in + head;
-    constexpr int UNR = GP <= 4 ? TFTB_CONE_UNR : 1;
+    constexpr int UNR = GP <= 4 ? 2 : 1;
     for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
         typename V::T buf[UNR][GP];
 #pragma unroll
@@ -1147,14 +962,8 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
     for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
 }
 
-#ifndef TFTB_CLG_NT
-#define TFTB_CLG_NT 256
-#endif
-#ifndef TFTB_CLG_MINB
-#define TFTB_CLG_MINB kern_minb<F>()
-#endif
 template <class F, int CL, int GAM>
-__global__ void __launch_bounds__(TFTB_CLG_NT, TFTB_CLG_MINB) k_clg_fwd(LaunchArgs<F> a) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);

@@ -44,12 +44,12 @@ extern "C" int tftb_debug_intt_tile(uint64_t p, uint64_t top, int K, void* data,
     }
 }
 
-// Phase timestamps on a uniform batch (count vectors of length n in the
-// cluster range): out[cta*8 + k] from the kernels' TFTB_STAMP points.
-// inverse = 1: k_cl_inv; otherwise the no-cluster forward k_clg_fwd.
+// Phase timestamps of the forward cluster-range kernel on a uniform batch
+// (count vectors of length n): out[cta*8 + k] from its TFTB_STAMP points.
 extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* data, int64_t n, int64_t count,
                                          unsigned long long* out, int inverse) {
     using namespace tftb;
+    if (inverse) return fail("debug: the split inverse has no phase stamps (time its two launches instead)");
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
     if (rh->kind != 0) return fail("debug: F30 only");
@@ -65,7 +65,10 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     a.timing = out;
     constexpr int CL = Limits<F30>::CL;
     const size_t smem = padded_words(1u << CL) * 4;
-    if (set_smem(k_cl_inv<F30, CL>, smem)) return -1;
+    const int gam = pl.l - CL;
+    void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
+                                 : gam == 2 ? k_clg_fwd<F30, CL, 2> : k_clg_fwd<F30, CL, 3>;
+    if (set_smem(kg, smem)) return -1;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(pl.G, (unsigned)count, 1);
     lc.blockDim = dim3(256, 1, 1);
@@ -77,16 +80,7 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    if (inverse != 1) {  // the no-cluster forward the dispatcher uses
-        const int gam = pl.l - CL;
-        void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
-                                     : gam == 2 ? k_clg_fwd<F30, CL, 2> : k_clg_fwd<F30, CL, 3>;
-        if (set_smem(kg, smem)) return -1;
-        lc.blockDim = dim3(TFTB_CLG_NT, 1, 1);
-        CK(cudaLaunchKernelEx(&lc, kg, a));
-    } else {
-        CK(cudaLaunchKernelEx(&lc, k_cl_inv<F30, CL>, a));
-    }
+    CK(cudaLaunchKernelEx(&lc, kg, a));
     CK(cudaDeviceSynchronize());
     return 0;
 }

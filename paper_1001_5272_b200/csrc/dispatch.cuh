@@ -143,44 +143,40 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     if (pl.kind == kCluster) {
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
-        const int nt = kNT;
-        auto ki = k_cl_inv<F, CL>;
-        if (set_smem(ki, smem)) return -1;
+        const int gam = pl.l - CL;
+        void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
+                                   : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
+        if (inverse ? (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem))
+                    : set_smem(kg, smem))
+            return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
-            cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3(pl.G, nv, 1);
-            lc.blockDim = dim3(nt, 1, 1);
-            lc.dynamicSmemBytes = smem;
-            lc.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = pl.G;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            static const bool split = !getenv("TFTB_INV_SPLIT") || atoi(getenv("TFTB_INV_SPLIT"));
-            if (inverse && split) {
-                if (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem)) return -1;
+            if (inverse) {
+                // split inverse: per-chunk launch, then one CTA per vector
                 k_cli_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
                 CK(cudaGetLastError());
                 k_cli_cols<F, CL><<<nv, kNT, smem, st>>>(a);
                 CK(cudaGetLastError());
-                g_launches++;
-            } else if (inverse) {
-                CK(cudaLaunchKernelEx(&lc, ki, a));
+                g_launches += 2;
             } else {
-                // forward: rows re-read through L2 instead of DSMEM (cluster only for the store barrier)
-                const int gam = pl.l - CL;
-                void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
-                                           : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
-                if (set_smem(kg, smem)) return -1;
-                lc.blockDim = dim3(TFTB_CLG_NT, 1, 1);
+                // forward: rows re-read through L2; the G CTAs of a vector form
+                // a cluster only for the split barrier ordering in-place stores
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3(pl.G, nv, 1);
+                lc.blockDim = dim3(kNT, 1, 1);
+                lc.dynamicSmemBytes = smem;
+                lc.stream = st;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = pl.G;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
                 CK(cudaLaunchKernelEx(&lc, kg, a));
+                g_launches++;
             }
-            g_launches++;
         }
         return 0;
     }
@@ -369,8 +365,7 @@ int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaS
     // stash, no scratch) fork onto side streams so one launch's tail wave
     // overlaps the next one's start; the join keeps `st` ordered after all
     // (graph-capture safe: fork/join through events).
-    static const bool fork_ok = !getenv("TFTB_GROUP_STREAMS") || atoi(getenv("TFTB_GROUP_STREAMS"));
-    bool fork = fork_ok && P->groups.size() > 1;
+    bool fork = P->groups.size() > 1;
     for (const auto& g : P->groups) {
         Plan pl;
         if (make_plan<F>(g.maxn, &pl)) return -1;

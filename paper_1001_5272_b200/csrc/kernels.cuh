@@ -25,12 +25,6 @@
 #pragma once
 #include "tile.cuh"
 
-#ifndef TFTB_LOAD_UNR
-#define TFTB_LOAD_UNR 8
-#endif
-#ifndef TFTB_CONE_UNR
-#define TFTB_CONE_UNR 2
-#endif
 
 template <typename W>
 struct VecDesc {
@@ -102,7 +96,7 @@ TFT_DEV T ld_stream(const T* p) { return __ldcs(p); }  // read once: evict-first
 // S[phys(i)] = xf(i, i < avail ? src[i] : 0) for i < C (phys(i) = i + i/32),
 // with 16-byte loads for the aligned body and UNR of them in flight per thread
 // (a tile load is one HBM latency, not C/blockDim of them).
-template <typename W, int UNR = TFTB_LOAD_UNR, class XF>
+template <typename W, int UNR = 8, class XF>
 TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& xf, Lanes ln = cta_lanes()) {
     using V = Vec16<W>;
     constexpr int NV = V::N;

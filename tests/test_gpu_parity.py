@@ -343,3 +343,32 @@ def test_device_footprint_audit():
         T.itft(x, cfg)
         peaks.append(backend.aux_bytes())
     assert max(peaks) <= 2 ** 14 * 4 + 32768, peaks  # one chunk stash + p2r partial sums
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["p998244353", "p3221225473", "p4179340454199820289"])
+def test_cluster_range_every_chunk_count_against_oracle(golden, key):
+    """The chunked plans (forward cone + split inverse) on every word type:
+    G = 2..8 chunks, complete last chunk (h = 0) and ragged ones, in a
+    ragged device batch and through the host API."""
+    cfg = cfg_for(golden, key)
+    C = 1 << (14 if cfg.p < 2 ** 32 else 13)
+    lens = []
+    for G in range(2, 9):
+        lens += [G * C, (G - 1) * C + 1, (G - 1) * C + C // 2 + 3, G * C - 1]
+    lens = np.array(lens, dtype=np.int64)
+    rng = np.random.default_rng(77)
+    flat = rng.integers(0, cfg.p, int(lens.sum()), dtype=np.uint64)
+    d = device.to_words(flat, cfg)
+    device.tft_batch_(d, cfg, lengths=lens)
+    got = device.from_words(d, cfg)
+    assert np.array_equal(got, O.tft_batch(flat, lens, cfg.p, cfg.omegaK, cfg.K))
+    device.tft_batch_(d, cfg, lengths=lens, inverse=True)
+    assert np.array_equal(device.from_words(d, cfg), flat)
+    # inverse of arbitrary words (not a forward image) against the oracle
+    z = rng.integers(0, cfg.p, int(lens[:8].sum()), dtype=np.uint64)
+    dz = device.to_words(z, cfg)
+    device.tft_batch_(dz, cfg, lengths=lens[:8], inverse=True)
+    off = np.concatenate([[0], np.cumsum(lens[:8])])
+    want = np.concatenate([O.itft(z[off[i]:off[i + 1]], cfg.p, cfg.omegaK, cfg.K) for i in range(8)])
+    assert np.array_equal(device.from_words(dz, cfg), want)

@@ -10,7 +10,7 @@ f.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, c
 names = {0: ["load", "sync1", "cross", "sync2", "rounds", "store", "-"],
          2: ["cone load", "sync", "-", "-", "rounds", "store", "-"],
          1: ["load", "intt", "sync1", "col1+publish", "exit sync", "phases23", "col2"]}
-for inv in [int(x) for x in os.environ.get('DIAG_DIRS', '1').split(',')]:
+for inv in [2]:  # forward only (the split inverse has no phase stamps)
     for n in [int(x) for x in sys.argv[1:]] or (40000, 49152, 57344, 65536):
         cnt = 4096
         G = (n + 16383) // 16384

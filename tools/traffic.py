@@ -5,9 +5,10 @@
         python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e
     python tools/traffic.py traffic.csv > profiles/traffic.json
 
-The last four tftb200 launches are the timed step (two forward size-class
-launches, then two inverse ones); ncu serialises and cold-starts them, so the
-bytes are the evidence here, not the times.
+The last six tftb200 launches are the timed step (two forward size-class
+launches, then per size class the split inverse's k_cli_chunks and
+k_cli_cols); ncu serialises and cold-starts them, so the bytes are the
+evidence here, not the times.
 """
 import csv
 import json
@@ -24,19 +25,20 @@ for r in rows[start + 1:]:
         continue
     d = launches.setdefault(r[ii], {"kernel": r[ki].split("(")[0]})
     d[r[mi]] = float(r[vi].replace(",", ""))
-ours = [d for d in launches.values() if d["kernel"].split("<")[0].split()[-1] in ("k_clg_fwd", "k_cl_inv")][-4:]
+ours = [d for d in launches.values()
+        if d["kernel"].split("<")[0].split()[-1] in ("k_clg_fwd", "k_cli_chunks", "k_cli_cols")][-6:]
 out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                 "--clock-control none (cold, serialised) on bench.py --steps 1 --warmup 3; last 4 tftb "
+                 "--clock-control none (cold, serialised) on bench.py --steps 1 --warmup 3; last 6 tftb "
                  "launches = the timed step",
        "launches": [{"kernel": d["kernel"], "ns": d["gpu__time_duration.sum"],
                      "dram_read": d["dram__bytes_read.sum"], "dram_write": d["dram__bytes_write.sum"]}
                     for d in ours]}
 tot = lambda ds: sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds)
-inv = [d for d in ours if "k_cl_inv" in d["kernel"]]
+inv = [d for d in ours if "k_cli_" in d["kernel"]]
 out["config2_bytes_per_step"] = tot(ours)
 out["config2_read_bytes"] = sum(d["dram__bytes_read.sum"] for d in ours)
 out["config2_write_bytes"] = sum(d["dram__bytes_write.sum"] for d in ours)
 out["inverse_pass_bytes"] = tot(inv)
-out["inverse_pass_kernel"] = inv[0]["kernel"] if inv else None
+out["inverse_pass_kernel"] = "k_cli_chunks + k_cli_cols"
 out["config2_ncu_step_ns"] = sum(d["gpu__time_duration.sum"] for d in ours)
 print(json.dumps(out, indent=1))
