@@ -384,9 +384,9 @@ TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typen
         // REDC dot products over raw Montgomery entries, <= 4 terms per reduction
 #pragma unroll
         for (int r = 0; r < M; ++r) {
-            W acc = 0;
+            W acc = redc_dot4(f, y, blkM + 8 * r, M);  // canonical
 #pragma unroll
-            for (int c0 = 0; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, y + c0, blkM + 8 * r + c0, M - c0));
+            for (int c0 = 4; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, y + c0, blkM + 8 * r + c0, M - c0));
             xv[r] = acc;
         }
     } else {
@@ -401,8 +401,9 @@ TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typen
     if (nv) {
         W acc = 0;
         if constexpr (std::is_same<F, F30>::value) {
+            acc = redc_dot4(f, xv, blkM + 64, M);
 #pragma unroll
-            for (int c0 = 0; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, xv + c0, blkM + 64 + c0, M - c0));
+            for (int c0 = 4; c0 < M; c0 += 4) acc = f.cadd(acc, redc_dot4(f, xv + c0, blkM + 64 + c0, M - c0));
         } else {
 #pragma unroll
             for (int c = 0; c < M; ++c) acc = f.cadd(acc, f.cmulw(xv[c], blk[64 + c]));
