@@ -105,29 +105,30 @@ TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& 
     for (uint32_t i = ln.id; i < head; i += ln.n) S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
     const uint32_t nq = (C - head) / NV;
     const typename V::T* vs = reinterpret_cast<const typename V::T*>(src + head);
-    for (uint32_t k0 = ln.id; k0 < nq; k0 += ln.n * UNR) {
+    // quads [0, nfull) lie wholly below avail: no per-word checks there
+    const int64_t rest = avail - (int64_t)head;
+    const uint32_t nfull = rest <= 0 ? 0u : (uint32_t)min((int64_t)nq, rest / NV);
+    for (uint32_t k0 = ln.id; k0 < nfull; k0 += ln.n * UNR) {
         typename V::T buf[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             const uint32_t k = k0 + u * ln.n;
-            const int64_t i = head + (int64_t)k * NV;
-            if (k < nq && i + NV <= avail) {
-                buf[u] = ld_stream(vs + k);
-            } else {
-                W e[NV];
-#pragma unroll
-                for (int q = 0; q < NV; ++q) e[q] = (k < nq && i + q < avail) ? src[i + q] : W(0);
-                buf[u] = V::make(e);
-            }
+            if (k < nfull) buf[u] = ld_stream(vs + k);
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             const uint32_t k = k0 + u * ln.n;
-            if (k >= nq) break;
+            if (k >= nfull) break;
             const uint32_t i = head + k * NV;
 #pragma unroll
             for (int q = 0; q < NV; ++q) S[(i + q) + ((i + q) >> 5)] = xf(i + q, V::get(buf[u], q));
         }
+    }
+    // the (at most one) partial quad and the zero quads past avail
+    for (uint32_t k = nfull + ln.id; k < nq; k += ln.n) {
+        const uint32_t i = head + k * NV;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) S[(i + q) + ((i + q) >> 5)] = xf(i + q, (int64_t)(i + q) < avail ? src[i + q] : W(0));
     }
     for (uint32_t i = head + nq * NV + ln.id; i < C; i += ln.n)
         S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
