@@ -219,11 +219,18 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
                     uint32_t col = g & (ncols - 1), i = i0 + (g >> tl.wlog);
                     W tv = tl.at(tl.ix(B + H + i, col));
-                    W lo = f.canon(tl.at(tl.ix(B + i, col)));
-                    W m = f.cmulw(tv, w);
-                    W x = f.csub(lo, m);
-                    tl.at(tl.ix(B + i, col)) = x;
-                    tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
+                    if constexpr (F::kLazy) {  // values stay in [0, 4p)
+                        const W m = f.mulw(tv, w);
+                        const W x = f.red2(tl.at(tl.ix(B + i, col))) - m + f.p2;
+                        tl.at(tl.ix(B + i, col)) = x;
+                        tl.at(tl.ix(B + H + i, col)) = f.red2(x) - m + f.p2;
+                    } else {
+                        W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                        W m = f.cmulw(tv, w);
+                        W x = f.csub(lo, m);
+                        tl.at(tl.ix(B + i, col)) = x;
+                        tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
+                    }
                 }
             } else {
                 const uint32_t cnt = (H - hd) << tl.wlog;
@@ -231,7 +238,8 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                     uint32_t col = g & (ncols - 1), i = hd + (g >> tl.wlog);
                     W a = tl.at(tl.ix(B + i, col));
                     W b = tl.at(tl.ix(B + H + i, col));
-                    tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
+                    if constexpr (F::kLazy) tl.at(tl.ix(B + i, col)) = f.red2(a) + f.mulw(b, w);
+                    else tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
                 }
             }
         }
@@ -248,10 +256,17 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                 const Tw<W> wh = cnt ? f.tw(f.twmul(w, R.inv2)) : w;  // w / 2: one product per element
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
                     uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
-                    W lo = f.canon(tl.at(tl.ix(B + i, col)));
-                    W hi = tl.at(tl.ix(B + H + i, col));
-                    tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                    tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.csub(lo, hi), wh);
+                    if constexpr (F::kLazy) {
+                        const W lo = f.red2(tl.at(tl.ix(B + i, col)));
+                        const W hi = f.red2(tl.at(tl.ix(B + H + i, col)));
+                        tl.at(tl.ix(B + i, col)) = f.mulw(lo + hi, R.inv2);
+                        tl.at(tl.ix(B + H + i, col)) = f.mulw(lo - hi + f.p2, wh);
+                    } else {
+                        W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                        W hi = tl.at(tl.ix(B + H + i, col));
+                        tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
+                        tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.csub(lo, hi), wh);
+                    }
                 }
             } else {
                 const uint32_t cnt = hd << tl.wlog;
@@ -259,7 +274,8 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                     uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
                     W a = tl.at(tl.ix(B + i, col));
                     W b = tl.at(tl.ix(B + H + i, col));
-                    tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
+                    if constexpr (F::kLazy) tl.at(tl.ix(B + i, col)) = f.red2(a) - f.mulw(b, w) + f.p2;
+                    else tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
                 }
             }
         }
