@@ -257,7 +257,11 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
     pre_d.n0 = H;
     // blocks per vector: ~8 per SM over the whole batch (full occupancy for a
     // streaming pass; per-thread setup is a few table loads)
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(8 * 148, (8 * 148 + count - 1) / count));
+    // and at least 16 1024-word rows per block, so a block's fixed cost
+    // (setup, reduction tree, ticket) stays small against its streaming
+    // (single 2^22 + 1 vector: -9%)
+    const int64_t rows = (H + r + 1023) / 1024;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>({8 * 148, (8 * 148 + count - 1) / count, rows / 16}));
     const Tw<W>* tab = p2r_tables<F>(rh, k, r, nb);
     if (!tab) return -1;
     const int64_t vchunk = 65535;
