@@ -963,6 +963,152 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
     for (uint32_t i = head + nq * NV + threadIdx.x; i < C; i += blockDim.x) one(i);
 }
 
+// Split forward (no cluster), two launches:
+// A (k_clf_cols, one CTA per vector): every column's 2^GAM-point network
+//   over the G rows (one read of the vector); rows < K (complete chunks) go
+//   back in place, row K (the last chunk, virtual words included) stays in
+//   shared memory and is transformed right there, only its first h outputs
+//   stored.  All of the vector's reads precede its writes in this one CTA.
+// B (k_clf_chunks, grid (G, vectors)): complete chunks g < K run their CL
+//   stages (sub-block g) on the column outputs.
+// Used where the cone forward's clusters cost the most (see dispatch).
+template <class F, int GAM>
+TFT_DEV void col_net(const F& f, typename F::W* v, const Tw<typename F::W>* tw) {
+    // v[r], r < 2^GAM: canonical inputs of one column -> outputs in [0, 4p)
+    // (lazy fields) or canonical (F32).  Stage sp pairs rows (r, r + 2^sp)
+    // with twiddle omega_{2 (r >> (sp+1))} = tw[r >> (sp+1)]; the top one is 1.
+    using W = typename F::W;
+    constexpr int GP = 1 << GAM;
+#pragma unroll
+    for (int sp = GAM - 1; sp >= 0; --sp) {
+#pragma unroll
+        for (int r = 0; r < GP; ++r) {
+            if (r & (1 << sp)) continue;
+            const int u = r + (1 << sp);
+            if constexpr (F::kLazy) {
+                if (sp == GAM - 1) {  // theta = 1 on canonical inputs: [0, 2p)
+                    const W a = v[r], b = v[u];
+                    v[r] = a + b;
+                    v[u] = a - b + f.p;
+                } else {
+                    const W a = sp == GAM - 2 ? v[r] : f.red2(v[r]);
+                    const W b = f.mulw(v[u], tw[r >> (sp + 1)]);
+                    v[r] = a + b;
+                    v[u] = a - b + f.p2;
+                }
+            } else {
+                f.fwd(v[r], v[u], tw[r >> (sp + 1)]);
+            }
+        }
+    }
+}
+
+template <class F, int CL, int GAM>
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_clf_cols(LaunchArgs<F> a) {
+    using W = typename F::W;
+    using V = Vec16<W>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    constexpr int GP = 1 << GAM, NV = V::N;
+    const int64_t v = a.vbase + blockIdx.x;
+    const int64_t n = a.xd.n(v), nin = a.ind.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v);
+    const W* in = a.in + a.ind.o(v);
+    Tw<W> tw[GP / 2];
+#pragma unroll
+    for (int k = 0; k < GP / 2; ++k) tw[k] = a.R.Zf[k];
+    uint32_t len[GP];  // words present in input row j
+#pragma unroll
+    for (int j = 0; j < GP; ++j) {
+        const int64_t r = nin - (int64_t)j * C;
+        len[j] = r <= 0 ? 0u : (uint32_t)min(r, (int64_t)C);
+    }
+    auto emit = [&](uint32_t c, const W* col) {
+#pragma unroll
+        for (int r = 0; r < GP; ++r) {
+            if ((uint32_t)r < K) x[(size_t)r * C + c] = col[r];
+            else if ((uint32_t)r == K && h) S[c + (c >> 5)] = col[r];
+        }
+    };
+    auto one = [&](uint32_t c) {
+        W col[GP];
+#pragma unroll
+        for (int j = 0; j < GP; ++j) col[j] = c < len[j] ? in[(size_t)j * C + c] : W(0);
+        col_net<F, GAM>(f, col, tw);
+        emit(c, col);
+    };
+    // input rows share the alignment of `in`, output rows that of `x`:
+    // 16-byte quads where both agree (always, for a transform in place)
+    const uint32_t mis_i = (uint32_t)(((uintptr_t)in & 15) / sizeof(W));
+    const uint32_t mis_x = (uint32_t)(((uintptr_t)x & 15) / sizeof(W));
+    const uint32_t head = mis_i == mis_x ? (NV - mis_i) % NV : C;
+    for (uint32_t c = threadIdx.x; c < head; c += blockDim.x) one(c);
+    const uint32_t nq = head < C ? (C - head) / NV : 0;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const uint32_t c0 = head + q * NV;
+        typename V::T buf[GP];
+#pragma unroll
+        for (int j = 0; j < GP; ++j) {
+            const W* src = in + (size_t)j * C + c0;
+            if (c0 + NV <= len[j]) {
+                buf[j] = __ldcs(reinterpret_cast<const typename V::T*>(src));  // read once
+            } else if (c0 >= len[j]) {
+                buf[j] = V::zero();
+            } else {
+                W e[NV];
+#pragma unroll
+                for (int k = 0; k < NV; ++k) e[k] = c0 + k < len[j] ? src[k] : W(0);
+                buf[j] = V::make(e);
+            }
+        }
+        W out[GP][NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            W col[GP];
+#pragma unroll
+            for (int j = 0; j < GP; ++j) col[j] = V::get(buf[j], k);
+            col_net<F, GAM>(f, col, tw);
+#pragma unroll
+            for (int r = 0; r < GP; ++r) out[r][k] = col[r];
+        }
+#pragma unroll
+        for (int r = 0; r < GP; ++r) {
+            if ((uint32_t)r < K) {
+                __stcg(reinterpret_cast<typename V::T*>(x + (size_t)r * C + c0), V::make(out[r]));
+            } else if ((uint32_t)r == K && h) {
+#pragma unroll
+                for (int k = 0; k < NV; ++k) S[(c0 + k) + ((c0 + k) >> 5)] = out[r][k];
+            }
+        }
+    }
+    for (uint32_t c = head + nq * NV + threadIdx.x; c < C && head < C; c += blockDim.x) one(c);
+    if (!h) return;
+    __syncthreads();
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, K, CL, f, a.R.ZfM}, h);
+    tile_store<W>(x + (size_t)K * C, S, h, [&](W w) { return f.canon(w); });
+}
+
+template <class F, int CL>
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_clf_chunks(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    constexpr uint32_t C = 1u << CL;
+    const uint32_t g = blockIdx.x;
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    if (((int64_t)g + 1) * C > n) return;  // complete chunks only
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v) + (size_t)g * C;
+    tile_load<W>(S, x, C, C, [](uint32_t, W w) { return w; });
+    __syncthreads();
+    fwd_rounds_ct<F, CL, CL, 0, true>(f, S, TwDirect<F>{a.R.Zf, g, CL, f, a.R.ZfM}, C);
+    tile_store<W>(x, S, C, [&](W w) { return f.canon(w); });
+}
+
 template <class F, int CL, int GAM>
 __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;

@@ -146,8 +146,15 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         const int gam = pl.l - CL;
         void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
                                    : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
+        void (*kf)(LaunchArgs<F>) = gam == 1 ? k_clf_cols<F, CL, 1>
+                                   : gam == 2 ? k_clf_cols<F, CL, 2> : k_clf_cols<F, CL, 3>;
+        // forward: the cone kernel needs a G-CTA cluster (in-place order);
+        // co-scheduling clusters costs most where the CTAs' lengths differ
+        // most -- 2 chunks (the partial one often tiny) and 5+ -- so those
+        // take the split forward (measured)
+        const bool fsplit = pl.G == 2 || pl.G >= 5;
         if (inverse ? (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem))
-                    : set_smem(kg, smem))
+                    : fsplit ? (set_smem(kf, smem) || set_smem(k_clf_chunks<F, CL>, smem)) : set_smem(kg, smem))
             return -1;
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
@@ -157,6 +164,12 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
                 k_cli_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
                 CK(cudaGetLastError());
                 k_cli_cols<F, CL><<<nv, kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+                g_launches += 2;
+            } else if (fsplit) {
+                kf<<<nv, kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+                k_clf_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
                 CK(cudaGetLastError());
                 g_launches += 2;
             } else {
