@@ -270,8 +270,7 @@ TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const T
             reg_inv<F, KK, 0, false>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
         }
         if constexpr (MASK) {
-            // only rows < h change; the rest is not written back, so another
-            // CTA may fill the tail [h, 2^TL) concurrently (k_cli_cols' column solve)
+            // only rows < h change; the rest is not written back
 #pragma unroll
             for (int i = 0; i < (1 << KK); ++i)
                 if (base + ((uint32_t)i << SLO) < h) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
@@ -570,8 +569,6 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> 
     const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
     W* x = a.x + a.xd.o(v);
     const F f = a.f;
-    if (h) tile_load<W>(S, x + (size_t)K * C, h, C, [](uint32_t, W w) { return w; });
-    __syncthreads();
     const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
     const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
     switch (K) {  // columns >= h: K rows
@@ -585,6 +582,9 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> 
 #undef TFTB_C1
     }
     if (!h) return;
+    // the last chunk's known outputs [0, h) (its tail [h, C) came from the
+    // column solve above: no zero fill)
+    tile_load<W>(S, x + (size_t)K * C, h, h, [](uint32_t, W w) { return w; });
     __syncthreads();
     const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
     itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
