@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F
     W* x = a.x + o;
     const F f = a.f;
     if (a.pre)
-        tile_load<W>(S, x + cbase, n - cbase, C, [&](uint32_t i, W w) { return load_pre(a, o + cbase + i, w); });
+        tile_load_pre<F>(a, S, x + cbase, a.pre + o + cbase, n - cbase, C);
     else
         tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_chunk_inv(LaunchArgs<F>
     const int64_t o = a.xd.o(v) + (int64_t)k * C;
     W* x = a.x + o;
     if (a.pre)
-        tile_load<W>(S, x, len, C, [&](uint32_t i, W w) { return load_pre(a, o + i, w); });
+        tile_load_pre<F>(a, S, x, a.pre + o, len, C);
     else
         tile_load<W>(S, x, len, C, [](uint32_t, W w) { return w; });
     __syncthreads();

@@ -62,11 +62,15 @@ __device__ __forceinline__ unsigned long long gtime() {
             (a).timing[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtime();                 \
     } while (0)
 
+// X^ * Y^ : Montgomery product then * R^2 to undo the R^-1.
+template <class F>
+TFT_DEV typename F::W pre_mul(const LaunchArgs<F>& a, typename F::W v, typename F::W pw) {
+    return a.f.canon(a.f.mont(a.f.red1(a.f.mont(v, pw)), a.R.r2w));
+}
 template <class F>
 TFT_DEV typename F::W load_pre(const LaunchArgs<F>& a, int64_t idx, typename F::W v) {
     if (!a.pre) return v;
-    // X^ * Y^ : Montgomery product then * R^2 to undo the R^-1.
-    return a.f.canon(a.f.mont(a.f.red1(a.f.mont(v, a.pre[idx])), a.R.r2w));
+    return pre_mul(a, v, a.pre[idx]);
 }
 
 // ------------------------------------------------------ tile <-> HBM streaming
@@ -132,6 +136,51 @@ TFT_DEV void tile_load(W* S, const W* src, int64_t avail, uint32_t C, const XF& 
     }
     for (uint32_t i = head + nq * NV + ln.id; i < C; i += ln.n)
         S[i + (i >> 5)] = xf(i, (int64_t)i < avail ? src[i] : W(0));
+}
+
+// tile_load of the pointwise product src[i] * pre[i] (the product's fused
+// inverse input): both operands in 16-byte quads, issued together, when
+// they share their alignment (the product's two buffers do); else the
+// scalar second operand of load_pre.
+template <class F, int UNR = 4>
+TFT_DEV void tile_load_pre(const LaunchArgs<F>& a, typename F::W* S, const typename F::W* src,
+                           const typename F::W* pre, int64_t avail, uint32_t C, Lanes ln = cta_lanes()) {
+    using W = typename F::W;
+    using V = Vec16<W>;
+    constexpr int NV = V::N;
+    const uint32_t mis = (uint32_t)(((uintptr_t)src & 15) / sizeof(W));
+    if (mis != (uint32_t)(((uintptr_t)pre & 15) / sizeof(W))) {
+        tile_load<W>(S, src, avail, C, [&](uint32_t i, W w) { return (int64_t)i < avail ? pre_mul(a, w, pre[i]) : W(0); }, ln);
+        return;
+    }
+    const uint32_t head = min(C, (uint32_t)((NV - mis) % NV));
+    auto one = [&](uint32_t i) { S[i + (i >> 5)] = (int64_t)i < avail ? pre_mul(a, src[i], pre[i]) : W(0); };
+    for (uint32_t i = ln.id; i < head; i += ln.n) one(i);
+    const uint32_t nq = (C - head) / NV;
+    const int64_t rest = avail - (int64_t)head;
+    const uint32_t nfull = rest <= 0 ? 0u : (uint32_t)min((int64_t)nq, rest / NV);
+    const typename V::T* vs = reinterpret_cast<const typename V::T*>(src + head);
+    const typename V::T* vp = reinterpret_cast<const typename V::T*>(pre + head);
+    for (uint32_t k0 = ln.id; k0 < nfull; k0 += ln.n * UNR) {
+        typename V::T bx[UNR], bp[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t k = k0 + u * ln.n;
+            if (k < nfull) {
+                bx[u] = ld_stream(vs + k);
+                bp[u] = ld_stream(vp + k);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const uint32_t k = k0 + u * ln.n;
+            if (k >= nfull) break;
+            const uint32_t i = head + k * NV;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) S[(i + q) + ((i + q) >> 5)] = pre_mul(a, V::get(bx[u], q), V::get(bp[u], q));
+        }
+    }
+    for (uint32_t i = head + nfull * NV + ln.id; i < C; i += ln.n) one(i);
 }
 
 // dst[i] = cv(S[phys(i)]) for i < lim, 16-byte stores for the aligned body

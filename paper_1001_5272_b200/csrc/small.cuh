@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_inv(LaunchArgs<F> 
         n = a.xd.n(v);
         o = a.xd.o(v);
         if (a.pre)
-            tile_load<W>(S, a.x + o, n, 1u << T, [&](uint32_t i, W w) { return load_pre(a, o + i, w); }, ln);
+            tile_load_pre<F>(a, S, a.x + o, a.pre + o, n, 1u << T, ln);
         else
             tile_load<W>(S, a.x + o, n, 1u << T, [](uint32_t, W w) { return w; }, ln);
     }
