@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
 // inverse steps 2 (which = 0: columns c >= h, K rows, stash their row K) and
 // 4 (which = 1: columns c < h, K+1 rows).  grid: (C >> WLOG, vectors)
 template <class F, int L0>
-__global__ void __launch_bounds__(256) k_colc_inv(LaunchArgs<F> a, int which) {
+__global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> a, int which) {
     using W = typename F::W;
     constexpr int WLOG = col_wlog<F, L0>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
