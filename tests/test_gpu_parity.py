@@ -372,3 +372,16 @@ def test_cluster_range_every_chunk_count_against_oracle(golden, key):
     off = np.concatenate([[0], np.cumsum(lens[:8])])
     want = np.concatenate([O.itft(z[off[i]:off[i + 1]], cfg.p, cfg.omegaK, cfg.K) for i in range(8)])
     assert np.array_equal(device.from_words(dz, cfg), want)
+
+
+@pytest.mark.gpu
+def test_products_in_the_chunked_range_against_oracle():
+    """Products whose length r uses the chunked plans (forward cone or split
+    forward, split inverse with the pointwise factor fused into its load)."""
+    cfg = T.default_config()
+    for la, lb in ((10, 16400), (20000, 20001), (30000, 35537), (70000, 40000), (1, 65536)):
+        a = gen(la, cfg.p, la)
+        b = gen(lb + 1, cfg.p, lb)
+        out = np.zeros(la + lb - 1, dtype=np.uint64)
+        T.multiply(a, b, out, cfg)
+        assert np.array_equal(out, O.multiply(a, b, cfg.p, cfg.omegaK, cfg.K)), (la, lb)
