@@ -170,7 +170,8 @@ def cpu_reference(lens, flat, reps=3, budget_vectors=None):
             "sample": f"first {nvec} of the 4096 config-2 vectors ({coeffs} coefficients), fwd and inv "
                       f"each best of {reps}, ThreadPoolExecutor({cores}) over vectors "
                       f"({'oracle/_ref = reference _kernels.pyx compiled' if mod else 'oracle C port'})",
-            "fwd_gcoeff_s": coeffs / best_f / 1e9, "inv_gcoeff_s": coeffs / best_i / 1e9}
+            "fwd_gcoeff_s": coeffs / best_f / 1e9, "inv_gcoeff_s": coeffs / best_i / 1e9,
+            "sample_ms_per_step": (best_f + best_i) * 1e3}
 
 
 # ------------------------------------------------------------------ main
@@ -197,7 +198,8 @@ def main():
         # each step is one bounded sample; best-of over `steps` runs
         res = cpu_reference(lens, flat, reps=max(1, args.steps))
         line = {"metric": "tft_itft_gcoeff_per_s", "value": res["value"], "unit": "Gcoeff/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": res["sample_ms_per_step"],  # one step = TFT + ITFT of the bounded sample
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (pinned numpy PCG64 generator, seed 1)", "impl": "reference",
                 "config": {"workload": "config2: 4096 x n in [2^15+1, 2^16], p=998244353, TFT+ITFT",
