@@ -133,7 +133,7 @@ def ref_module():
     return mod
 
 
-def cpu_reference(lens, flat, reps=3, budget_vectors=None):
+def cpu_reference(lens, flat, reps=3, budget_vectors=None, warm=0):
     """Time the reference's compiled kernels (or the oracle port) on a sample
     of the batch, threaded over vectors on all host cores."""
     from oracle import oracle as O
@@ -163,6 +163,9 @@ def cpu_reference(lens, flat, reps=3, budget_vectors=None):
             list(ex.map(one, bufs))
         return time.perf_counter() - t0
 
+    for _ in range(warm):  # untimed warm-up steps
+        run("fwd")
+        run("inv")
     best_f = min(run("fwd") for _ in range(reps))
     best_i = min(run("inv") for _ in range(reps))
     gcs = 2 * coeffs / (best_f + best_i) / 1e9
@@ -196,7 +199,7 @@ def main():
             return
         lens, flat = c2_batch(1)
         # each step is one bounded sample; best-of over `steps` runs
-        res = cpu_reference(lens, flat, reps=max(1, args.steps))
+        res = cpu_reference(lens, flat, reps=max(1, args.steps), warm=args.warmup)
         line = {"metric": "tft_itft_gcoeff_per_s", "value": res["value"], "unit": "Gcoeff/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": res["sample_ms_per_step"],  # one step = TFT + ITFT of the bounded sample
