@@ -348,15 +348,6 @@ TFT_DEV void inv_rounds_ct(const F& f, typename F::W* S, const TP& tp, const Tw<
     }
 }
 
-// this CTA's share [lo, hi) of the columns [c0, C), 32-aligned
-__device__ __forceinline__ void col_share(uint32_t c0, uint32_t C, uint32_t g, uint32_t G, uint32_t& lo,
-                                          uint32_t& hi) {
-    const uint32_t span = C - c0;
-    lo = c0 + ((uint32_t)(((uint64_t)span * g / G)) & ~31u);
-    hi = g + 1 == G ? C : c0 + ((uint32_t)(((uint64_t)span * (g + 1) / G)) & ~31u);
-    if (g == 0) lo = c0;
-}
-
 // dot product of M canonical words with M Montgomery words, reduced once:
 // the raw 64-bit products accumulate exactly while their sum stays below
 // p 2^32 (<= 4 terms for p < 2^30), then one REDC gives the value
@@ -445,22 +436,6 @@ TFT_DEV void col_solve_range(const F& f, const LD& ld, const NX& nx, typename F:
 #pragma unroll
         for (int j = 0; j < M; ++j) y[j] = ld(j, c);
         one(c, y);
-    }
-}
-
-template <class F, class LD, class NX>
-TFT_DEV void col_solve(const F& f, const LD& ld, const NX& nx, typename F::W* xg, uint32_t C, uint32_t lo,
-                       uint32_t hi, int m, const Tw<typename F::W>* blk, const typename F::W* blkM,
-                       bool write_next) {
-    switch (m) {
-        case 1: col_solve_range<F, 1>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 2: col_solve_range<F, 2>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 3: col_solve_range<F, 3>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 4: col_solve_range<F, 4>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 5: col_solve_range<F, 5>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 6: col_solve_range<F, 6>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        case 7: col_solve_range<F, 7>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
-        default: col_solve_range<F, 8>(f, ld, nx, xg, C, lo, hi, blk, blkM, write_next); break;
     }
 }
 
