@@ -73,13 +73,15 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     lc.gridDim = dim3(pl.G, (unsigned)count, 1);
     lc.blockDim = dim3(256, 1, 1);
     lc.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = pl.G;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    at[1].val.clusterSchedulingPolicyPreference = cudaClusterSchedulingPolicyLoadBalancing;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = 2;
     CK(cudaLaunchKernelEx(&lc, kg, a));
     CK(cudaDeviceSynchronize());
     return 0;

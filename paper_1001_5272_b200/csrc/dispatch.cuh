@@ -149,10 +149,9 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         void (*kf)(LaunchArgs<F>) = gam == 1 ? k_clf_cols<F, CL, 1>
                                    : gam == 2 ? k_clf_cols<F, CL, 2> : k_clf_cols<F, CL, 3>;
         // forward: the cone kernel needs a G-CTA cluster (in-place order);
-        // co-scheduling clusters costs most where the CTAs' lengths differ
-        // most -- 2 chunks (the partial one often tiny) and 5+ -- so those
-        // take the split forward (measured)
-        const bool fsplit = pl.G == 2 || pl.G >= 5;
+        // from 5 chunks on, co-scheduling such clusters costs more than the
+        // split forward's second pass (measured)
+        const bool fsplit = pl.G >= 5;
         if (inverse ? (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem))
                     : fsplit ? (set_smem(kf, smem) || set_smem(k_clf_chunks<F, CL>, smem)) : set_smem(kg, smem))
             return -1;
@@ -180,13 +179,18 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
                 lc.blockDim = dim3(kNT, 1, 1);
                 lc.dynamicSmemBytes = smem;
                 lc.stream = st;
-                cudaLaunchAttribute at[1];
+                cudaLaunchAttribute at[2];
                 at[0].id = cudaLaunchAttributeClusterDimension;
                 at[0].val.clusterDim.x = pl.G;
                 at[0].val.clusterDim.y = 1;
                 at[0].val.clusterDim.z = 1;
                 lc.attrs = at;
                 lc.numAttrs = 1;
+                // let the hardware place a cluster's CTAs on any free SMs of
+                // the GPC (measured: config-2 forward -5%, 2-chunk vectors -25%)
+                at[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+                at[1].val.clusterSchedulingPolicyPreference = cudaClusterSchedulingPolicyLoadBalancing;
+                lc.numAttrs = 2;
                 CK(cudaLaunchKernelEx(&lc, kg, a));
                 g_launches++;
             }
