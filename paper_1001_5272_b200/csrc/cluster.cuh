@@ -659,16 +659,13 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_last_inv(LaunchArgs<F> 
 // r 2^l1 + c.  One CTA owns 2^WLOG adjacent columns of 2^L0 rows.
 template <class F>
 __host__ __device__ constexpr int col_tile_log() { return sizeof(typename F::W) == 4 ? 14 : 13; }
-// adjacent columns per CTA: a 2^col_tile_log-word tile, at most 2^MAXW
-// columns (the inverse's per-column sums split a column over
-// blockDim >> WLOG threads: MAXW 8; the forward has no such step: up to 2^10,
-// so short columns still fill a 64 KB tile and keep enough bytes in flight)
-template <class F, int L0, int MAXW = 8>
-__host__ __device__ constexpr int col_wlog() {
-    return (col_tile_log<F>() - L0) < 0 ? 0 : ((col_tile_log<F>() - L0) > MAXW ? MAXW : (col_tile_log<F>() - L0));
-}
+// adjacent columns per CTA: a 2^col_tile_log-word tile, at most 2^10
+// columns, so short columns still fill a 64 KB tile and keep enough bytes
+// in flight (= host.h make_plan's wlog)
 template <class F, int L0>
-__host__ __device__ constexpr int col_wlog_fwd() { return col_wlog<F, L0, 10>(); }
+__host__ __device__ constexpr int col_wlog() {
+    return (col_tile_log<F>() - L0) < 0 ? 0 : ((col_tile_log<F>() - L0) > 10 ? 10 : (col_tile_log<F>() - L0));
+}
 
 // S[(r << WLOG) | col] = xf(r, col, valid ? src[r*C + col] : 0), valid = r*C + col < avail;
 // 16-byte loads along rows when the rows are 16-byte aligned, UNR in flight.
@@ -720,7 +717,7 @@ TFT_DEV void col_load(W* S, const W* src, uint32_t C, int64_t avail, const XF& x
 template <class F, int L0>
 __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
-    constexpr int WLOG = col_wlog_fwd<F, L0>();
+    constexpr int WLOG = col_wlog<F, L0>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
     const int64_t v = a.vbase + blockIdx.y;

@@ -211,10 +211,9 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     Scratch stash;
     if (!stash_buf && stash.get((size_t)std::min(count, vchunk) * C * sizeof(W), st, true)) return -1;
     a.stash = stash_buf ? stash_buf : (W*)stash.p;
-    const size_t sm_col = padded_words(1u << (pl.l0 + pl.wlog)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
-    // the forward column kernel's tiles may be wider (col_wlog_fwd)
-    const int wlog_f = std::max(0, std::min(10, Limits<F>::col_t - pl.l0));
-    const size_t sm_colf = padded_words(1u << (pl.l0 + wlog_f)) * sizeof(W) + (kNT + 256 + 8) * sizeof(W);
+    // column tile + the inverse's per-column sums (blockDim words of partials,
+    // one word per column)
+    const size_t sm_col = (padded_words(1u << (pl.l0 + pl.wlog)) + kNT + (1u << pl.wlog) + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
     // compile-time column kernels, one instantiation per l0
     void (*colf)(LaunchArgs<F>) = nullptr;
@@ -230,8 +229,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
 #undef TFTB_COL
         default: return fail("no column kernel for this plan");
     }
-    if (pl.wlog != std::max(0, std::min(8, Limits<F>::col_t - pl.l0))) return fail("column plan mismatch");
-    if (set_smem(colf, sm_colf) || set_smem(coli, sm_col)) return -1;
+    if (pl.wlog != std::max(0, std::min(10, Limits<F>::col_t - pl.l0))) return fail("column plan mismatch");
+    if (set_smem(colf, sm_col) || set_smem(coli, sm_col)) return -1;
     // chunk kernels for this plan's chunk size (2^CL, or 2^14 for the u64 words
     // past 2^26, make_plan)
     auto chunks = [&](auto cl) -> int {
@@ -242,9 +241,9 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         for (int64_t v0 = 0; v0 < count; v0 += vchunk) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min(count - v0, vchunk);
-            dim3 gcol(C >> pl.wlog, nv), gcolf(C >> wlog_f, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
+            dim3 gcol(C >> pl.wlog, nv), gchunk((unsigned)maxchunks, nv), glast(1, nv);
             if (!inverse) {
-                colf<<<gcolf, kNT, sm_colf, st>>>(a);
+                colf<<<gcol, kNT, sm_col, st>>>(a);
                 k_chunk_fwd<F, CLK><<<gchunk, kNT, sm_chunk, st>>>(a);
                 g_launches += 2;
             } else {

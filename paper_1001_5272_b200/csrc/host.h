@@ -163,8 +163,8 @@ int make_plan(int64_t n, Plan* pl, bool p2r_ok = true) {
         l0 = l - l1;
         col_max = 14;
     }
-    // up to 256 adjacent columns (colsum_pow needs blockDim >= columns)
-    int wlog = std::max(0, std::min(8, Limits<F>::col_t - l0));
+    // up to 1024 adjacent columns (a 64 KB tile for 16-row columns)
+    int wlog = std::max(0, std::min(10, Limits<F>::col_t - l0));
     if (l0 + wlog > col_max) return fail("transform length too large for the two-pass plan");
     pl->l0 = l0;
     pl->l1 = l1;

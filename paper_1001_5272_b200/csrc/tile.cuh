@@ -292,6 +292,16 @@ TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t 
                         typename F::W one, typename F::W* red, typename F::W* out) {
     using W = typename F::W;
     const uint32_t ncols = 1u << tl.wlog;
+    if (ncols >= blockDim.x) {  // wide tiles: whole columns per thread, Horner over the K rows
+        const Tw<W> w = f.tw(wword);
+        for (uint32_t col = threadIdx.x; col < ncols; col += blockDim.x) {
+            W acc = 0;
+            for (uint32_t i = K; i-- > 0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(i, col))));
+            out[col] = acc;
+        }
+        __syncthreads();
+        return;
+    }
     const uint32_t nparts = blockDim.x >> tl.wlog;
     const uint32_t col = threadIdx.x & (ncols - 1), part = threadIdx.x >> tl.wlog;
     const uint32_t e = (K + nparts - 1) / nparts;
