@@ -668,49 +668,69 @@ __host__ __device__ constexpr int col_wlog() {
 }
 
 // S[(r << WLOG) | col] = xf(r, col, valid ? src[r*C + col] : 0), valid = r*C + col < avail;
-// 16-byte loads along rows when the rows are 16-byte aligned, UNR in flight.
+// 16-byte loads along rows, UNR in flight.  Every row shares the alignment
+// of src (C is a multiple of the vector), so the columns [head, head + 4 nqr)
+// are whole quads in every row; the few columns before and after go scalar.
 template <typename W, int L0, int WLOG, int UNR = 8, class XF>
 TFT_DEV void col_load(W* S, const W* src, uint32_t C, int64_t avail, const XF& xf) {
     constexpr int NV = 16 / sizeof(W);
     constexpr uint32_t R = 1u << L0, NC = 1u << WLOG;
-    const bool vec = (NC % NV == 0) && (((uintptr_t)src & 15) == 0) && (C % NV == 0);
-    if (vec) {
-        constexpr uint32_t QPR = NC / NV;  // quads per row
-        const uint32_t nq = R * QPR;
-        for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
-            typename Vec16<W>::T buf[UNR];
+    auto put = [&](uint32_t r, uint32_t c, W w) {
+        const uint32_t idx = (r << WLOG) | c;
+        S[idx + (idx >> 5)] = xf(r, c, w);
+    };
+    const uint32_t mis = (uint32_t)(((uintptr_t)src & 15) / sizeof(W));
+    const uint32_t head = (C % NV) ? NC : min(NC, (uint32_t)((NV - mis) % NV));
+    // quads per row: NC/NV when aligned, one fewer otherwise (compile-time
+    // divisors either way)
+    constexpr uint32_t QA = NC / NV, QM = QA > 0 ? QA - 1 : 0;
+    auto quads = [&](auto nqr_c) {
+        constexpr uint32_t NQR = decltype(nqr_c)::value;
+        if constexpr (NQR > 0) {
+            constexpr uint32_t nq = R * NQR;
+            for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
+                typename Vec16<W>::T buf[UNR];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t q = q0 + u * blockDim.x;
-                const uint32_t r = q / QPR, c = (q % QPR) * NV;
-                const int64_t pos = (int64_t)r * C + c;
-                if (q < nq && pos + NV <= avail) {
-                    buf[u] = ld_stream(reinterpret_cast<const typename Vec16<W>::T*>(src + pos));
-                } else {
-                    W e[NV];
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t q = q0 + u * blockDim.x;
+                    const uint32_t r = q / NQR, c = head + (q % NQR) * NV;
+                    const int64_t pos = (int64_t)r * C + c;
+                    if (q < nq && pos + NV <= avail) {
+                        buf[u] = ld_stream(reinterpret_cast<const typename Vec16<W>::T*>(src + pos));
+                    } else {
+                        W e[NV];
 #pragma unroll
-                    for (int k = 0; k < NV; ++k) e[k] = (q < nq && pos + k < avail) ? src[pos + k] : W(0);
-                    buf[u] = Vec16<W>::make(e);
+                        for (int k = 0; k < NV; ++k) e[k] = (q < nq && pos + k < avail) ? src[pos + k] : W(0);
+                        buf[u] = Vec16<W>::make(e);
+                    }
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint32_t q = q0 + u * blockDim.x;
-                if (q >= nq) break;
-                const uint32_t r = q / QPR, c = (q % QPR) * NV;
+                for (int u = 0; u < UNR; ++u) {
+                    const uint32_t q = q0 + u * blockDim.x;
+                    if (q >= nq) break;
+                    const uint32_t r = q / NQR, c = head + (q % NQR) * NV;
 #pragma unroll
-                for (int k = 0; k < NV; ++k) {
-                    const uint32_t idx = (r << WLOG) | (c + k);
-                    S[idx + (idx >> 5)] = xf(r, c + k, Vec16<W>::get(buf[u], k));
+                    for (int k = 0; k < NV; ++k) put(r, c + k, Vec16<W>::get(buf[u], k));
                 }
             }
         }
+    };
+    uint32_t tail;
+    if (head == 0) {
+        quads(std::integral_constant<uint32_t, QA>{});
+        tail = QA * NV;
+    } else if (head < NC) {
+        quads(std::integral_constant<uint32_t, QM>{});
+        tail = head + QM * NV;
     } else {
-        for (uint32_t g = threadIdx.x; g < (R << WLOG); g += blockDim.x) {
-            const uint32_t r = g >> WLOG, c = g & (NC - 1);
-            const int64_t pos = (int64_t)r * C + c;
-            S[g + (g >> 5)] = xf(r, c, pos < avail ? src[pos] : W(0));
-        }
+        tail = NC;
+    }
+    // the edge columns [0, head) and [tail, NC) of every row
+    const uint32_t ne = head + (NC - tail);
+    for (uint32_t g = threadIdx.x; g < R * ne; g += blockDim.x) {
+        const uint32_t r = g / ne, j = g % ne, c = j < head ? j : tail + (j - head);
+        const int64_t pos = (int64_t)r * C + c;
+        put(r, c, pos < avail ? src[pos] : W(0));
     }
 }
 
