@@ -544,6 +544,8 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> 
     const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
     W* x = a.x + a.xd.o(v);
     const F f = a.f;
+    // stream the vector into L2 (TMA bulk prefetch) while the first quads load
+    if (threadIdx.x == 0) l2_prefetch(x, n);
     const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
     const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
     switch (K) {  // columns >= h: K rows
@@ -782,6 +784,11 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     const uint32_t rows = which == 0 ? K : K + 1;
     const F f = a.f;
     W* x = a.x + a.xd.o(v);
+    // the tile's row segments into L2 (TMA bulk prefetch), one per thread
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+        const int64_t b = (int64_t)r * C + c0;
+        if (b < n) l2_prefetch(x + b, min((int64_t)NC, n - b));
+    }
     col_load<W, L0, WLOG>(S, x + c0, C, n - c0, [&](uint32_t r, uint32_t, W w) { return r < rows ? w : W(0); });
     __syncthreads();
     const TwPrefix<F> tpf{a.R.Zf}, tpi{a.R.Zi};

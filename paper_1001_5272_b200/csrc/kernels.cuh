@@ -62,6 +62,20 @@ __device__ __forceinline__ unsigned long long gtime() {
             (a).timing[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 + (k)] = gtime();                 \
     } while (0)
 
+// Hint: bring words [p, p + words) into L2 with TMA bulk prefetches (the
+// copy engine streams them while the SM works).  Only the 16-byte-aligned
+// inner span, so it never touches bytes outside the range.
+template <typename W>
+TFT_DEV void l2_prefetch(const W* p, int64_t words) {
+    if (words <= 0) return;
+    uintptr_t lo = ((uintptr_t)p + 15) & ~(uintptr_t)15;
+    const uintptr_t hi = ((uintptr_t)(p + words)) & ~(uintptr_t)15;
+    for (; lo < hi; lo += 32768) {
+        const uint32_t sz = (uint32_t)min((uintptr_t)32768, hi - lo);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(sz) : "memory");
+    }
+}
+
 // X^ * Y^ : Montgomery product then * R^2 to undo the R^-1.
 template <class F>
 TFT_DEV typename F::W pre_mul(const LaunchArgs<F>& a, typename F::W v, typename F::W pw) {
