@@ -784,10 +784,14 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     const uint32_t rows = which == 0 ? K : K + 1;
     const F f = a.f;
     W* x = a.x + a.xd.o(v);
-    // the tile's row segments into L2 (TMA bulk prefetch), one per thread
-    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-        const int64_t b = (int64_t)r * C + c0;
-        if (b < n) l2_prefetch(x + b, min((int64_t)NC, n - b));
+    // the tile's row segments into L2 (TMA bulk prefetch), one per thread --
+    // only when they are long (short columns, wide tiles): thousands of tiny
+    // segments cost more than they hide (single 2^25-word vectors: +7%)
+    if constexpr (((1u << WLOG) * sizeof(W)) >= 1024) {
+        for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+            const int64_t b = (int64_t)r * C + c0;
+            if (b < n) l2_prefetch(x + b, min((int64_t)NC, n - b));
+        }
     }
     col_load<W, L0, WLOG>(S, x + c0, C, n - c0, [&](uint32_t r, uint32_t, W w) { return r < rows ? w : W(0); });
     __syncthreads();
