@@ -905,7 +905,7 @@ TFT_DEV typename F::W cone_row_ct(const F& f, typename F::W* vals, const Tw<type
 // alignment: scalar head, then quads -- per row a quad is full, empty or
 // (at most once per row) partial, decided on 32-bit offsets against the
 // row's precomputed length -- then a scalar tail.
-template <class F, int CL, int GAM, int GI>
+template <class F, int CL, int GAM, int GI, int NR = (1 << GAM)>
 TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, int64_t nin,
                        const Tw<typename F::W>* Zf) {
     using W = typename F::W;
@@ -921,12 +921,13 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
 #pragma unroll
     for (int j = 0; j < GP; ++j) {
         const int64_t r = nin - (int64_t)j * C - head;
-        len[j] = r <= 0 ? 0u : (uint32_t)min(r, (int64_t)C);
+        // rows >= NR (the vector has NR chunks) are known zeros at compile time
+        len[j] = j >= NR || r <= 0 ? 0u : (uint32_t)min(r, (int64_t)C);
     }
     auto one = [&](uint32_t i) {
         W vals[GP];
 #pragma unroll
-        for (int j = 0; j < GP; ++j) vals[j] = (int64_t)j * C + i < nin ? in[(size_t)j * C + i] : W(0);
+        for (int j = 0; j < GP; ++j) vals[j] = j < NR && (int64_t)j * C + i < nin ? in[(size_t)j * C + i] : W(0);
         S[i + (i >> 5)] = cone_row_ct<F, GAM, GI>(f, vals, tw);
     };
     for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) one(i);
@@ -1118,7 +1119,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clf_chunks(LaunchArgs<F
     tile_store<W>(x, S, C, [&](W w) { return f.canon(w); });
 }
 
-template <class F, int CL, int GAM>
+template <class F, int CL, int GAM, int NR = (1 << GAM)>
 __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1140,14 +1141,14 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a
     const W* in = a.in + a.ind.o(v);
     TFTB_STAMP(a, 0);
     switch (g) {  // the cone's half selections are compile-time per CTA
-        case 0: cone_fill<F, CL, GAM, 0>(f, S, in, nin, a.R.Zf); break;
-        case 1: cone_fill<F, CL, GAM, 1>(f, S, in, nin, a.R.Zf); break;
-        case 2: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 2>(f, S, in, nin, a.R.Zf); break;
-        case 3: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 3>(f, S, in, nin, a.R.Zf); break;
-        case 4: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 4>(f, S, in, nin, a.R.Zf); break;
-        case 5: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 5>(f, S, in, nin, a.R.Zf); break;
-        case 6: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 6>(f, S, in, nin, a.R.Zf); break;
-        default: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 7>(f, S, in, nin, a.R.Zf); break;
+        case 0: cone_fill<F, CL, GAM, 0, NR>(f, S, in, nin, a.R.Zf); break;
+        case 1: cone_fill<F, CL, GAM, 1, NR>(f, S, in, nin, a.R.Zf); break;
+        case 2: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 2, NR>(f, S, in, nin, a.R.Zf); break;
+        case 3: if constexpr (GAM >= 2) cone_fill<F, CL, GAM, 3, NR>(f, S, in, nin, a.R.Zf); break;
+        case 4: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 4, NR>(f, S, in, nin, a.R.Zf); break;
+        case 5: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 5, NR>(f, S, in, nin, a.R.Zf); break;
+        case 6: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 6, NR>(f, S, in, nin, a.R.Zf); break;
+        default: if constexpr (GAM >= 3) cone_fill<F, CL, GAM, 7, NR>(f, S, in, nin, a.R.Zf); break;
     }
     TFTB_STAMP(a, 1);
     // In place (in == x), chunk g is also a row of every sibling CTA's

@@ -144,8 +144,10 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         constexpr int CL = Limits<F>::CL;
         const size_t smem = padded_words(1u << CL) * sizeof(W);
         const int gam = pl.l - CL;
+        // (the chunk count is a template argument: rows past it are known zeros)
         void (*kg)(LaunchArgs<F>) = gam == 1 ? k_clg_fwd<F, CL, 1>
-                                   : gam == 2 ? k_clg_fwd<F, CL, 2> : k_clg_fwd<F, CL, 3>;
+                                   : gam == 2 ? (pl.G == 3 ? k_clg_fwd<F, CL, 2, 3> : k_clg_fwd<F, CL, 2>)
+                                              : k_clg_fwd<F, CL, 3>;
         void (*kf)(LaunchArgs<F>) = gam == 1 ? k_clf_cols<F, CL, 1>
                                    : gam == 2 ? k_clf_cols<F, CL, 2> : k_clf_cols<F, CL, 3>;
         // forward: the cone kernel needs a G-CTA cluster (in-place order);
