@@ -385,3 +385,38 @@ def test_products_in_the_chunked_range_against_oracle():
         out = np.zeros(la + lb - 1, dtype=np.uint64)
         T.multiply(a, b, out, cfg)
         assert np.array_equal(out, O.multiply(a, b, cfg.p, cfg.omegaK, cfg.K)), (la, lb)
+
+
+@pytest.mark.gpu
+def test_concurrent_calls_on_distinct_buffers():
+    """The reference's concurrency model: calls on distinct buffers may run
+    at once (its kernels release the GIL; ctypes does too).  Several host
+    threads transform, invert and multiply their own buffers together."""
+    import threading
+    cfg = T.default_config()
+    errors = []
+
+    def worker(k):
+        try:
+            for r in range(3):
+                n = [1000, 40000, 70001, 2 ** 20 + 1][(k + r) % 4]
+                x = gen(100 * k + r, cfg.p, n)
+                y = x.copy()
+                T.tft(y, cfg)
+                if n <= 70001:
+                    assert np.array_equal(y, O.tft(x, cfg.p, cfg.omegaK, cfg.K)), n
+                T.itft(y, cfg)
+                assert np.array_equal(y, x), n
+                a, b = gen(k, cfg.p, 3000 + k), gen(k + 50, cfg.p, 2000)
+                out = np.zeros(a.size + b.size - 1, dtype=np.uint64)
+                T.multiply(a, b, out, cfg)
+                assert np.array_equal(out, O.multiply(a, b, cfg.p, cfg.omegaK, cfg.K))
+        except Exception as e:  # noqa: BLE001  (reported below)
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
