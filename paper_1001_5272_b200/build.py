@@ -19,41 +19,77 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 OBJ = os.path.join(HERE, "csrc", "_obj")
 
 
-def _digest():
+def _deps(path, seen=None):
+    """The unit plus every local header it includes (transitively)."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for m in re.finditer(r'#include\s+"([^"]+)"', f.read()):
+            _deps(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
+
+
+def _unit_digest(unit):
     h = hashlib.sha256(" ".join(FLAGS).encode())
-    for d in (os.path.join(HERE, "csrc"), os.path.join(ROOT, "include")):
-        for name in sorted(os.listdir(d)):
-            if os.path.isdir(os.path.join(d, name)):
-                continue
-            with open(os.path.join(d, name), "rb") as f:
-                h.update(name.encode() + f.read())
+    for p in sorted(_deps(os.path.join(HERE, "csrc", unit))):
+        with open(p, "rb") as f:
+            h.update(os.path.basename(p).encode() + f.read())
+    return h.hexdigest()
+
+
+def _digest():
+    h = hashlib.sha256()
+    for u in UNITS:
+        h.update(_unit_digest(u).encode())
     return h.hexdigest()
 
 
 def build(force=False, verbose=False):
+    """Compile the units whose sources (or local headers) changed, then link."""
     dig = _digest()
     if not force and os.path.exists(OUT) and os.path.exists(STAMP):
         with open(STAMP) as f:
             if f.read().strip() == dig:
                 return OUT
     os.makedirs(OBJ, exist_ok=True)
-    procs = []
+    procs, objs = [], []
     for u in UNITS:
         obj = os.path.join(OBJ, u.replace(".cu", ".o"))
+        objs.append(obj)
+        ud = _unit_digest(u)
+        if not force and os.path.exists(obj) and os.path.exists(obj + ".stamp"):
+            with open(obj + ".stamp") as f:
+                if f.read().strip() == ud:
+                    continue
         cmd = [NVCC, *FLAGS, "-c", "-o", obj, os.path.join(HERE, "csrc", u)]
-        procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+        procs.append((obj, ud, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     log, failed = "", False
-    for obj, pr in procs:
+    for obj, ud, pr in procs:
         out, _ = pr.communicate()
         log += f"==== {obj}\n{out}"
-        failed |= pr.returncode != 0
+        if pr.returncode != 0:
+            failed = True
+        else:
+            with open(obj + ".stamp", "w") as f:
+                f.write(ud)
+            with open(obj + ".log", "w") as f:
+                f.write(out)
     if not failed:
-        link = subprocess.run([NVCC, "-shared", "-o", OUT, *[o for o, _ in procs], "-lcudart"],
+        link = subprocess.run([NVCC, "-shared", "-o", OUT, *objs, "-lcudart"],
                               capture_output=True, text=True)
         log += link.stdout + link.stderr
         failed = link.returncode != 0
+    # ptxas.log: every unit's latest register / spill report
+    full = ""
+    for obj in objs:
+        if os.path.exists(obj + ".log"):
+            with open(obj + ".log") as f:
+                full += f"==== {obj}\n{f.read()}"
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:
-        f.write(log)
+        f.write(full + (log if failed else ""))
     if failed:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed building libtftb200.so")

@@ -6,21 +6,7 @@
 
 namespace tftb {
 
-// side streams for concurrent plan groups (per device, created once)
-constexpr int kGroupStreams = 4;
-inline cudaStream_t* group_streams() {
-    static std::mutex mu;
-    static std::map<int, std::vector<cudaStream_t>> per_dev;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    auto& v = per_dev[dev];
-    if (v.empty()) {
-        v.resize(kGroupStreams);
-        for (auto& s : v) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    }
-    return v.data();
-}
+constexpr int kGroupStreams = 4;  // side streams per forking plan
 
 // whole-vector tiles of one size class T = ceil_lg(n)
 template <class F, int T>
@@ -114,6 +100,16 @@ const Tw<typename F::W>* p2r_tables(const RingHost* rh, int k, int r, int nb) {
         }
     }
     return (const Tw<W>*)d;
+}
+
+// blocks per vector of k_p2r: ~8 per SM over the whole batch (full
+// occupancy for a streaming pass; per-thread setup is a few table loads) and
+// at least 16 1024-word rows per block, so a block's fixed cost (setup,
+// reduction tree, ticket) stays small against its streaming (single 2^22 + 1
+// vector: -9%)
+inline int p2r_blocks(int64_t count, int64_t H, int r) {
+    const int64_t rows = (H + r + 1023) / 1024;
+    return (int)std::max<int64_t>(1, std::min<int64_t>({8 * 148, (8 * 148 + count - 1) / count, rows / 16}));
 }
 
 // n = 2^k + r: fold + r dot products + the 2^k transform (p2r.cuh)
@@ -276,13 +272,7 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
     VecDesc<W> pre_d = xd;  // the 2^k prefix of every vector
     pre_d.len = nullptr;
     pre_d.n0 = H;
-    // blocks per vector: ~8 per SM over the whole batch (full occupancy for a
-    // streaming pass; per-thread setup is a few table loads)
-    // and at least 16 1024-word rows per block, so a block's fixed cost
-    // (setup, reduction tree, ticket) stays small against its streaming
-    // (single 2^22 + 1 vector: -9%)
-    const int64_t rows = (H + r + 1023) / 1024;
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>({8 * 148, (8 * 148 + count - 1) / count, rows / 16}));
+    const int nb = p2r_blocks(count, H, r);
     const Tw<W>* tab = p2r_tables<F>(rh, k, r, nb);
     if (!tab) return -1;
     const int64_t vchunk = 65535;
@@ -342,10 +332,13 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
 
 template <class F>
 int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
-                const int64_t* h_len, PlanImpl* P) {
+                const int64_t* h_len, PlanImpl* P, cudaStream_t async_st, bool async,
+                bool allow_fork) {
     using W = typename F::W;
     P->rh = rh;
     P->count = count;
+    P->async = async;
+    P->async_st = async_st;
     std::map<int, std::vector<int64_t>> groups;
     for (int64_t v = 0; v < count; v++) {
         int64_t nv = h_len ? h_len[v] : n;
@@ -355,6 +348,7 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
         groups[pl.key()].push_back(v);
     }
     size_t words = 0, stash_words = 0;
+    bool fork = allow_fork && groups.size() > 1;
     for (auto& kv : groups) {
         PlanGroup g;
         g.count = (int64_t)kv.second.size();
@@ -371,15 +365,43 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
         if (pl.kind == kLarge || pl.kind == kP2R)  // (p2r: its 2^k prefix runs the two-pass plan;
             // chunks are 2^CL words, 2^14 for u64 words past 2^26)
             stash_words = std::max(stash_words, (size_t)std::min<int64_t>(g.count, 65535) << 14);
+        if (pl.kind == kP2R) {  // its power tables now, so execute only enqueues
+            const int k = pl.l - 1;
+            if (!p2r_tables<F>(rh, k, pl.G, p2r_blocks(g.count, 1ll << k, pl.G))) return -1;
+        }
+        fork &= pl.kind == kSmall || pl.kind == kCluster;
         g.arr_off = words;
         words += 2 * g.count;
         P->host_arrays.insert(P->host_arrays.end(), off.begin(), off.end());
         P->host_arrays.insert(P->host_arrays.end(), len.begin(), len.end());
         P->groups.push_back(g);
     }
-    CK(cudaMalloc(&P->darr, std::max<size_t>(words, 1) * sizeof(int64_t)));
-    CK(cudaMemcpy(P->darr, P->host_arrays.data(), words * sizeof(int64_t), cudaMemcpyHostToDevice));
-    if (stash_words) CK(cudaMalloc(&P->stash, stash_words * sizeof(W)));
+    const size_t abytes = std::max<size_t>(words, 1) * sizeof(int64_t);
+    if (async) {
+        // pageable source: cudaMemcpyAsync returns once it is staged
+        CK(cudaMallocAsync(&P->darr, abytes, async_st));
+        CK(cudaMemcpyAsync(P->darr, P->host_arrays.data(), words * sizeof(int64_t), cudaMemcpyHostToDevice,
+                           async_st));
+        if (stash_words) CK(cudaMallocAsync(&P->stash, stash_words * sizeof(W), async_st));
+    } else {
+        CK(cudaMalloc(&P->darr, abytes));
+        CK(cudaMemcpy(P->darr, P->host_arrays.data(), words * sizeof(int64_t), cudaMemcpyHostToDevice));
+        if (stash_words) CK(cudaMalloc(&P->stash, stash_words * sizeof(W)));
+    }
+    if (stash_words) {
+        g_aux_cur += (int64_t)(stash_words * sizeof(W));
+        g_aux_peak = std::max(g_aux_peak, g_aux_cur);
+        g_aux_cur -= (int64_t)(stash_words * sizeof(W));
+    }
+    P->fork = fork;
+    if (fork) {
+        const size_t ns = std::min<size_t>(P->groups.size(), kGroupStreams);
+        P->side.resize(ns);
+        for (auto& s2 : P->side) CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        P->ev_join.resize(P->groups.size());
+        for (auto& e : P->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     return 0;
 }
 
@@ -387,50 +409,32 @@ template <class F>
 int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st) {
     using W = typename F::W;
     // Groups are independent vectors.  Tile and cluster groups (no shared
-    // stash, no scratch) fork onto side streams so one launch's tail wave
-    // overlaps the next one's start; the join keeps `st` ordered after all
-    // (graph-capture safe: fork/join through events).
-    bool fork = P->groups.size() > 1;
-    for (const auto& g : P->groups) {
-        Plan pl;
-        if (make_plan<F>(g.maxn, &pl)) return -1;
-        fork &= pl.kind == kSmall || pl.kind == kCluster;
-    }
-    cudaStream_t* side = fork ? group_streams() : nullptr;
-    cudaEvent_t ev_fork = nullptr;
-    std::vector<cudaEvent_t> ev_join;
-    if (fork) {
-        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev_fork, st));
-    }
+    // stash, no scratch) fork onto the plan's side streams so one launch's
+    // tail wave overlaps the next one's start; the join keeps `st` ordered
+    // after all (fork/join through the plan's events: graph-capture safe).
+    if (P->fork) CK(cudaEventRecord(P->ev_fork, st));
     int rc = 0;
     for (size_t i = 0; i < P->groups.size() && !rc; ++i) {
         const auto& g = P->groups[i];
         const int64_t* d = (const int64_t*)P->darr + g.arr_off;
         VecDesc<W> xd{d, d + g.count, 0, 0};
         cudaStream_t gs = st;
-        if (fork) {
-            gs = side[i % kGroupStreams];
-            CK(cudaStreamWaitEvent(gs, ev_fork, 0));
+        if (P->fork) {
+            gs = P->side[i % P->side.size()];
+            CK(cudaStreamWaitEvent(gs, P->ev_fork, 0));
         }
         rc = run_group<F>(P->rh, (W*)data, nullptr, (const W*)pre, g.count, xd, xd, g.maxn, inverse != 0, gs,
                           (W*)P->stash);
-        if (fork) {
-            cudaEvent_t e;
-            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            CK(cudaEventRecord(e, gs));
-            ev_join.push_back(e);
-        }
+        if (P->fork) CK(cudaEventRecord(P->ev_join[i], gs));
     }
-    for (auto e : ev_join) {
-        CK(cudaStreamWaitEvent(st, e, 0));
-        cudaEventDestroy(e);
-    }
-    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (P->fork)
+        for (size_t i = 0; i < P->groups.size(); ++i) CK(cudaStreamWaitEvent(st, P->ev_join[i], 0));
     return rc;
 }
 
 // Partition a batch by plan (ceil_lg of the length class) and run each group.
+// Ragged batches build a temporary plan whose arrays are allocated, filled
+// and released stream-ordered on `st`: asynchronous w.r.t. the host.
 template <class F>
 int run_batch(const RingHost* rh, void* data, const void* in, int64_t count, int64_t n, int64_t stride,
               const int64_t* h_off, const int64_t* h_len, const void* in_data, int64_t in_n,
@@ -444,10 +448,8 @@ int run_batch(const RingHost* rh, void* data, const void* in, int64_t count, int
     }
     (void)in;
     PlanImpl P;
-    if (plan_create<F>(rh, count, n, stride, h_off, h_len, &P)) return -1;
-    int rc = plan_exec<F>(&P, data, inverse, pre, st);
-    CK(cudaStreamSynchronize(st));  // the temporary plan's arrays die here
-    return rc;
+    if (plan_create<F>(rh, count, n, stride, h_off, h_len, &P, st, true)) return -1;
+    return plan_exec<F>(&P, data, inverse, pre, st);
 }
 
 template <class F>
@@ -479,7 +481,7 @@ int dispatch_mul(const RingHost* rh, const void* a, int64_t la, int64_t sa, cons
 
 #define TFTB_INSTANTIATE(F)                                                                                   \
     template int tftb::plan_create<F>(const RingHost*, int64_t, int64_t, int64_t, const int64_t*, const int64_t*, \
-                                      PlanImpl*);                                                               \
+                                      PlanImpl*, cudaStream_t, bool, bool);                                                               \
     template int tftb::plan_exec<F>(const PlanImpl*, void*, int, const void*, cudaStream_t);                  \
     template int tftb::dispatch_tft<F>(const RingHost*, void*, int64_t, int64_t, int64_t, const int64_t*,     \
                                        const int64_t*, int, cudaStream_t);                                      \

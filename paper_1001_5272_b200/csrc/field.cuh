@@ -99,17 +99,27 @@ struct F30M : F30 {
     TFT_DEV explicit F30M(const F30& f) : F30(f) {}
     TFT_DEV W mulw(W b, Tw<W> t) const { return __umulhi(b, t.w) - __umulhi(b * t.wp, p) + p; }
     TFT_DEV W scale(W b, Tw<W> t) const { return F30::mulw(b, t); }
+    // Both outputs straight from hi = hi(y wR) and u = hi((y wRp) p):
+    // x = (ra + p) + hi - u, y = (ra + p) - hi + u (ra = red2(x)), the same
+    // words as a + b, a - b + 2p with b = hi - u + p.  Written this way
+    // ptxas keeps hi - u out of a 64-bit-addend IMAD.HI, whose zeroed and
+    // negated operand registers cost two extra FMA-pipe moves per product
+    // (tools/cu/engmix.cu: bottom round 6.7 -> 8.8 butterflies/clk/SM).
     TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
-        W a = red2(x);
-        W b = mulw(y, t);
-        x = a + b;
-        y = a - b + p2;
+        const W ra = red2(x) + p;
+        const W hi = __umulhi(y, t.w);
+        const W u = __umulhi(y * t.wp, p);
+        x = ra + hi - u;
+        y = ra - hi + u;
     }
+    // (x - y) w as one REDC of the 64-bit sum d wR + m p, m = d (-wRp):
+    // [0, 2p) (engmix: 7.4 -> 7.6)
     TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
-        W s = red2(x + y);
-        W d = x - y + p2;
+        const W s = red2(x + y);
+        const W d = x - y + p2;
         x = s;
-        y = mulw(d, t);
+        const W m = d * (0u - t.wp);
+        y = (W)(((uint64_t)d * t.w + (uint64_t)m * p) >> 32);
     }
 };
 
@@ -139,18 +149,22 @@ struct F32 {
     TFT_DEV Tw<W> tw(W wM) const { return Tw<W>{wM, wM * pinv}; }
     TFT_DEV W twmul(Tw<W> a, Tw<W> b) const { return mont(a.w, b.w); }
     TFT_DEV W scale(W b, Tw<W> t) const { return mulw(b, t); }
+    // a + b = a - (p - b): the borrow of the subtraction is the only test
+    // (one compare instead of the carry and range tests of a + b)
     TFT_DEV W cadd(W a, W b) const {
-        W s = a + b;
-        return (s < a || s >= p) ? s - p : s;
+        const W nb = p - b;
+        const W s = a - nb;
+        return a < nb ? s + p : s;
     }
     TFT_DEV W csub(W a, W b) const {
         W d = a - b;
         return a < b ? d + p : d;
     }
     TFT_DEV W cmulw(W b, Tw<W> t) const { return mulw(b, t); }
+    // (engmix: forward and inverse rounds +8% over the carry-test cadd)
     TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
-        W b = mulw(y, t);
-        W a = x;
+        const W b = mulw(y, t);
+        const W a = x;
         x = cadd(a, b);
         y = csub(a, b);
     }
@@ -160,10 +174,9 @@ struct F32 {
     }
     TFT_DEV W half1(W x, W y, bool sel) const { return sel ? csub(x, y) : cadd(x, y); }
     TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
-        W s = cadd(x, y);
-        W d = csub(x, y);
-        x = s;
-        y = mulw(d, t);
+        const W a = x, b = y;
+        x = cadd(a, b);
+        y = mulw(csub(a, b), t);
     }
 };
 

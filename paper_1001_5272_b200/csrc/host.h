@@ -219,6 +219,11 @@ struct PlanGroup {
     size_t arr_off;  // offsets then lengths, in darr
 };
 
+// A plan owns everything its execution touches besides the data: device
+// offset/length arrays, the stash, the p2r tables (built at creation) and,
+// when its groups fork, its own side streams and fork/join events -- so
+// execute only enqueues work (graph-capturable) and two plans never share
+// a stream.  A plan is not meant to be executed by two threads at once.
 struct PlanImpl {
     const RingHost* rh = nullptr;
     int64_t count = 0;
@@ -226,15 +231,33 @@ struct PlanImpl {
     std::vector<int64_t> host_arrays;
     void* darr = nullptr;
     void* stash = nullptr;
+    bool fork = false;
+    std::vector<cudaStream_t> side;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
+    // temporary plans (tftb_tft_dev with host offsets): arrays allocated and
+    // released stream-ordered on this stream, no host synchronisation
+    cudaStream_t async_st = nullptr;
+    bool async = false;
     ~PlanImpl() {
-        if (darr) cudaFree(darr);
-        if (stash) cudaFree(stash);
+        if (async) {
+            if (darr) cudaFreeAsync(darr, async_st);
+            if (stash) cudaFreeAsync(stash, async_st);
+        } else {
+            if (darr) cudaFree(darr);
+            if (stash) cudaFree(stash);
+        }
+        // (destroying a stream or event with pending work is legal: the
+        // resources go once the work completes)
+        for (auto e : ev_join) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        for (auto s : side) cudaStreamDestroy(s);
     }
 };
 
 template <class F>
 int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
-                const int64_t* h_len, PlanImpl* P);
+                const int64_t* h_len, PlanImpl* P, cudaStream_t async_st, bool async, bool allow_fork = true);
 template <class F>
 int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaStream_t st);
 

@@ -227,6 +227,76 @@ int get_ring(uint64_t p, uint64_t top, int K, RingHost** out) {
     return 0;
 }
 
+// ------------------------------------------------------------ host contexts
+// The host-pointer entry points run on a non-blocking stream leased from a
+// per-device pool: one per concurrently active caller thread.  Calls on
+// distinct buffers from different threads therefore overlap on the device,
+// as the reference's nogil kernels do on CPU cores (_kernels.pyx:419,428,453),
+// and nothing runs on the legacy default stream.  Device staging comes from
+// the stream-ordered pool (cached, get_ring sets its release threshold).
+struct HostCtx {
+    int dev;
+    cudaStream_t st;
+    // pinned staging for pageable caller buffers (grow-only, up to
+    // kPinMax): DMA from page-locked memory instead of the driver's shared
+    // bounce buffer, which serialises concurrent callers
+    void* pin = nullptr;
+    size_t pin_cap = 0;
+    int pin_reserve(size_t bytes) {
+        if (bytes <= pin_cap) return 0;
+        if (pin) cudaFreeHost(pin);
+        pin = nullptr;
+        pin_cap = 0;
+        size_t cap = std::max<size_t>(bytes, 1 << 20);
+        cap = (cap + (1 << 20) - 1) & ~(size_t)((1 << 20) - 1);
+        CK(cudaHostAlloc(&pin, cap, cudaHostAllocDefault));
+        pin_cap = cap;
+        return 0;
+    }
+};
+constexpr size_t kPinMax = 64u << 20;
+
+inline bool host_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+std::mutex g_ctx_mu;
+std::map<int, std::vector<HostCtx*>> g_ctx_free;
+
+struct CtxLease {
+    HostCtx* c = nullptr;
+    int acquire() {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        {
+            std::lock_guard<std::mutex> lk(g_ctx_mu);
+            auto& v = g_ctx_free[dev];
+            if (!v.empty()) {
+                c = v.back();
+                v.pop_back();
+                return 0;
+            }
+        }
+        std::unique_ptr<HostCtx> n(new HostCtx{dev, nullptr});
+        CK(cudaStreamCreateWithFlags(&n->st, cudaStreamNonBlocking));
+        c = n.release();
+        return 0;
+    }
+    cudaStream_t stream() const { return c->st; }
+    ~CtxLease() {
+        if (!c) return;
+        // nothing of this call may still touch the caller's buffers (error
+        // paths included) once it returns
+        cudaStreamSynchronize(c->st);
+        std::lock_guard<std::mutex> lk(g_ctx_mu);
+        g_ctx_free[c->dev].push_back(c);
+    }
+};
+
 // model op counts of the device algorithm
 int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, bool inverse, int64_t* mults,
                     int64_t* adds) {
@@ -234,12 +304,20 @@ int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, boo
     if (K < 62 && n > (1ll << K)) return fail("length exceeds 2^K");
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
-    cudaStream_t st = nullptr;
+    CtxLease lease;
+    if (lease.acquire()) return -1;
+    cudaStream_t st = lease.stream();
     const size_t wb = rh->wbytes;
     Scratch buf;
     if (buf.get((size_t)n * 8 + (wb == 4 ? (size_t)n * 4 : 0), st)) return -1;
     uint64_t* d64 = (uint64_t*)buf.p;
-    CK(cudaMemcpyAsync(d64, x, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    uint64_t* hx = x;
+    if ((size_t)n * 8 <= kPinMax && !host_pinned(x)) {
+        if (lease.c->pin_reserve((size_t)n * 8)) return -1;
+        hx = (uint64_t*)lease.c->pin;
+        memcpy(hx, x, (size_t)n * 8);
+    }
+    CK(cudaMemcpyAsync(d64, hx, (size_t)n * 8, cudaMemcpyHostToDevice, st));
     int rc = 0;
     if (wb == 4) {
         uint32_t* dw = (uint32_t*)(d64 + n);
@@ -254,8 +332,9 @@ int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, boo
         rc = dispatch_tft<F62>(rh, d64, 1, n, n, nullptr, nullptr, inverse, st);
         if (rc) return rc;
     }
-    CK(cudaMemcpyAsync(x, d64, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hx, d64, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (hx != x) memcpy(x, hx, (size_t)n * 8);
     tally_transform(n, p, K, inverse, mults, adds);
     return 0;
 }
@@ -286,7 +365,9 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     if (K < 62 && r > (1ll << K)) return fail("product length exceeds 2^K");
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
-    cudaStream_t st = nullptr;
+    CtxLease lease;
+    if (lease.acquire()) return -1;
+    cudaStream_t st = lease.stream();
     const size_t wb = rh->wbytes;
     // device: a, b, x as u64 staging + (u32 field) word copies + the Y scratch
     Scratch buf;
@@ -296,8 +377,21 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     uint64_t* db64 = da64 + la;
     uint64_t* dx64 = db64 + lb;
     unsigned char* wbase = (unsigned char*)(dx64 + r);
-    CK(cudaMemcpyAsync(da64, a, (size_t)la * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db64, b, (size_t)lb * 8, cudaMemcpyHostToDevice, st));
+    // pinned staging for pageable callers: [a | b | x]
+    const uint64_t* ha = a;
+    const uint64_t* hb = b;
+    uint64_t* hx = x;
+    if (words64 * 8 <= kPinMax && !(host_pinned(a) && host_pinned(b) && host_pinned(x))) {
+        if (lease.c->pin_reserve(words64 * 8)) return -1;
+        uint64_t* hp = (uint64_t*)lease.c->pin;
+        memcpy(hp, a, (size_t)la * 8);
+        memcpy(hp + la, b, (size_t)lb * 8);
+        ha = hp;
+        hb = hp + la;
+        hx = hp + la + lb;
+    }
+    CK(cudaMemcpyAsync(da64, ha, (size_t)la * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db64, hb, (size_t)lb * 8, cudaMemcpyHostToDevice, st));
     int rc;
     if (wb == 4) {
         uint32_t* da = (uint32_t*)wbase;
@@ -315,8 +409,9 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
         rc = dispatch_mul<F62>(rh, da64, la, la, db64, lb, lb, dx64, r, 1, dy, st);
         if (rc) return rc;
     }
-    CK(cudaMemcpyAsync(x, dx64, (size_t)r * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hx, dx64, (size_t)r * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (hx != x) memcpy(x, hx, (size_t)r * 8);
     tally_multiply(la, lb, p, K, mults, adds);
     return 0;
 }
@@ -325,10 +420,15 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
 
 namespace {
 
-// Host-batch pipeline: the batch is cut into sub-batches of consecutive
-// vectors; each sub-batch's H2D copy, word conversion, transform, conversion
-// back and D2H copy are issued on one of three streams, so PCIe traffic in
-// both directions overlaps the kernels of neighbouring sub-batches.
+// Host-batch pipeline.  The vectors (sorted by offset, non-overlapping) are
+// cut into sub-batches of consecutive vectors; sub-batch b runs on pipeline
+// slot b mod 3, each slot a stream with its own device staging of one
+// sub-batch: H2D of the sub-batch's vectors, packed back to back (one copy
+// per run of touching vectors -- words between vectors are never read or
+// written), u64 -> word conversion, the batch transform, conversion back,
+// D2H of the same runs.  PCIe traffic in both directions overlaps the
+// kernels of neighbouring sub-batches, and device memory is three
+// sub-batches' staging whatever the batch size.
 constexpr int kPipeStreams = 3;
 
 cudaStream_t* pipe_streams() {
@@ -344,54 +444,113 @@ cudaStream_t* pipe_streams() {
     }
     return v.data();
 }
+std::mutex g_pipe_mu;  // one host-batch pipeline at a time per process (its streams are shared)
+
+struct SubBatch {
+    int64_t v0, v1;                                // [v0, v1) in sorted order
+    int64_t words;                                 // packed words
+    std::vector<std::pair<int64_t, int64_t>> runs;  // (host word offset, words), packed in order
+};
 
 template <class F>
-int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64_t>& o, const int64_t* len,
-                        int64_t count, int64_t lo, int64_t span, int inverse) {
+int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64_t>& ord, const int64_t* off,
+                        const int64_t* len, int inverse) {
     using W = typename F::W;
     const bool narrow = sizeof(W) == 4;
-    Scratch buf;
-    if (buf.get((size_t)span * 8 + (narrow ? (size_t)span * 4 : 0), nullptr)) return -1;
-    CK(cudaStreamSynchronize(nullptr));
-    uint64_t* d64 = (uint64_t*)buf.p;
-    W* dw = narrow ? (W*)(d64 + span) : (W*)d64;
-    // sub-batches of ~span/48 words (at least 2^22), consecutive vectors:
-    // shorter pipeline fill and drain (measured: 12 -> 48 parts, +2% e2e)
-    const int64_t target = std::max<int64_t>(span / 48, 1 << 22);
-    std::vector<std::pair<int64_t, int64_t>> subs;
-    for (int64_t v0 = 0; v0 < count;) {
-        int64_t v1 = v0, words = 0;
-        while (v1 < count && (words < target || v1 == v0)) words += len[v1++];
-        subs.push_back({v0, v1});
-        v0 = v1;
+    const int64_t count = (int64_t)ord.size();
+    int64_t total = 0;
+    for (int64_t i = 0; i < count; i++) total += len[ord[i]];
+    // sub-batches of ~total/48 words (at least 2^22, at most 2^25 words
+    // unless one vector is longer): short pipeline fill and drain
+    // (measured: 12 -> 48 parts, +2% e2e)
+    const int64_t target = std::min<int64_t>(std::max<int64_t>(total / 48, 1 << 22), 1 << 25);
+    std::vector<SubBatch> subs;
+    int64_t maxw = 0;
+    for (int64_t i0 = 0; i0 < count;) {
+        SubBatch sb;
+        sb.v0 = i0;
+        sb.words = 0;
+        int64_t i1 = i0;
+        while (i1 < count && (sb.words < target || i1 == i0)) {
+            const int64_t v = ord[i1];
+            if (!sb.runs.empty() && sb.runs.back().first + sb.runs.back().second == off[v])
+                sb.runs.back().second += len[v];
+            else
+                sb.runs.push_back({off[v], len[v]});
+            sb.words += len[v];
+            i1++;
+        }
+        sb.v1 = i1;
+        maxw = std::max(maxw, sb.words);
+        subs.push_back(std::move(sb));
+        i0 = i1;
     }
-    std::vector<std::unique_ptr<PlanImpl>> plans;
-    for (auto& sb : subs) {
-        plans.emplace_back(new PlanImpl());
-        if (plan_create<F>(rh, sb.second - sb.first, 0, 0, o.data() + sb.first, len + sb.first, plans.back().get()))
-            return -1;
-    }
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
     cudaStream_t* ss = pipe_streams();
-    for (size_t b = 0; b < subs.size(); b++) {
+    // per-slot staging: u64 words (+ the word copy for u32 rings)
+    const size_t slot_bytes = ((size_t)maxw * (narrow ? 12 : 8) + 255) & ~(size_t)255;
+    Scratch buf;
+    if (buf.get(slot_bytes * kPipeStreams, ss[0])) return -1;
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, ss[0]));
+    for (int i = 1; i < kPipeStreams; i++) CK(cudaStreamWaitEvent(ss[i], ready, 0));
+    std::vector<std::unique_ptr<PlanImpl>> plans;
+    std::vector<int64_t> poff, plen;
+    for (auto& sb : subs) {
+        poff.clear();
+        plen.clear();
+        int64_t acc = 0;
+        for (int64_t i = sb.v0; i < sb.v1; i++) {
+            poff.push_back(acc);
+            plen.push_back(len[ord[i]]);
+            acc += len[ord[i]];
+        }
+        plans.emplace_back(new PlanImpl());
+        // (no forking: the pipeline's slots already overlap sub-batches, and
+        // per-plan side streams would cost a stream creation per sub-batch)
+        if (plan_create<F>(rh, sb.v1 - sb.v0, 0, 0, poff.data(), plen.data(), plans.back().get(), nullptr, false,
+                           false)) {
+            cudaEventDestroy(ready);
+            return -1;
+        }
+    }
+    int rc = 0;
+    for (size_t b = 0; b < subs.size() && !rc; b++) {
+        const SubBatch& sb = subs[b];
         cudaStream_t st = ss[b % kPipeStreams];
-        const int64_t a0 = o[subs[b].first];
-        const int64_t a1 = o[subs[b].second - 1] + len[subs[b].second - 1];
-        const int64_t nw = a1 - a0;
-        CK(cudaMemcpyAsync(d64 + a0, x + lo + a0, (size_t)nw * 8, cudaMemcpyHostToDevice, st));
-        const int nb = (int)std::min<int64_t>((nw + 255) / 256, 148 * 8);
+        uint64_t* d64 = (uint64_t*)((char*)buf.p + slot_bytes * (b % kPipeStreams));
+        W* dw = narrow ? (W*)(d64 + maxw) : (W*)d64;
+        int64_t at = 0;
+        for (auto& r : sb.runs) {
+            if (cudaMemcpyAsync(d64 + at, x + r.first, (size_t)r.second * 8, cudaMemcpyHostToDevice, st)) rc = -1;
+            at += r.second;
+        }
+        const int nb = (int)std::min<int64_t>((sb.words + 255) / 256, 148 * 8);
         if (narrow) {
-            k_u64_to_w<W><<<nb, 256, 0, st>>>(d64 + a0, dw + a0, nw);
+            k_u64_to_w<W><<<nb, 256, 0, st>>>(d64, dw, sb.words);
             g_launches++;
         }
-        if (plan_exec<F>(plans[b].get(), dw, inverse, nullptr, st)) return -1;
+        if (!rc && plan_exec<F>(plans[b].get(), dw, inverse, nullptr, st)) rc = -1;
         if (narrow) {
-            k_w_to_u64<W><<<nb, 256, 0, st>>>(dw + a0, d64 + a0, nw);
+            k_w_to_u64<W><<<nb, 256, 0, st>>>(dw, d64, sb.words);
             g_launches++;
         }
-        CK(cudaMemcpyAsync(x + lo + a0, d64 + a0, (size_t)nw * 8, cudaMemcpyDeviceToHost, st));
+        at = 0;
+        for (auto& r : sb.runs) {
+            if (cudaMemcpyAsync(x + r.first, d64 + at, (size_t)r.second * 8, cudaMemcpyDeviceToHost, st)) rc = -1;
+            at += r.second;
+        }
+        if (rc && g_err.empty()) fail(std::string("host batch copy: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    // the staging is released on slot 0 after every slot's work
+    for (int i = 1; i < kPipeStreams; i++) {
+        CK(cudaEventRecord(ready, ss[i]));
+        CK(cudaStreamWaitEvent(ss[0], ready, 0));
     }
     for (int i = 0; i < kPipeStreams; i++) CK(cudaStreamSynchronize(ss[i]));
-    return 0;
+    cudaEventDestroy(ready);
+    return rc;
 }
 
 }  // namespace
@@ -401,53 +560,29 @@ extern "C" {
 int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int64_t count, uint64_t p,
                        uint64_t top, int K, int inverse) {
     if (count <= 0) return 0;
-    if (!len) return fail("len must not be NULL");
+    if (!len || !x) return fail("x and len must not be NULL");
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
     std::vector<int64_t> o(count);
-    int64_t lo = INT64_MAX, hi = 0, acc = 0;
+    int64_t acc = 0;
     bool sorted = true;
     for (int64_t v = 0; v < count; v++) {
         if (len[v] <= 0 || (K < 62 && len[v] > (1ll << K))) return fail("vector length outside [1, 2^K]");
         o[v] = off ? off[v] : acc;
-        if (v && o[v] < o[v - 1] + len[v - 1]) sorted = false;
+        if (o[v] < 0) return fail("negative vector offset");
+        if (v && o[v] < o[v - 1]) sorted = false;
         acc += len[v];
-        lo = std::min(lo, o[v]);
-        hi = std::max(hi, o[v] + len[v]);
     }
-    const int64_t span = hi - lo;
-    for (auto& e : o) e -= lo;
-    if (sorted) {
-        switch (rh->kind) {
-            case 0: return host_batch_pipeline<F30>(rh, x, o, len, count, lo, span, inverse);
-            case 1: return host_batch_pipeline<F32>(rh, x, o, len, count, lo, span, inverse);
-            default: return host_batch_pipeline<F62>(rh, x, o, len, count, lo, span, inverse);
-        }
+    std::vector<int64_t> ord(count);
+    for (int64_t v = 0; v < count; v++) ord[v] = v;
+    if (!sorted) std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return o[a] < o[b]; });
+    for (int64_t i = 1; i < count; i++)
+        if (o[ord[i]] < o[ord[i - 1]] + len[ord[i - 1]]) return fail("vectors overlap");
+    switch (rh->kind) {
+        case 0: return host_batch_pipeline<F30>(rh, x, ord, o.data(), len, inverse);
+        case 1: return host_batch_pipeline<F32>(rh, x, ord, o.data(), len, inverse);
+        default: return host_batch_pipeline<F62>(rh, x, ord, o.data(), len, inverse);
     }
-    // overlapping / unsorted layouts: one stream, whole span
-    cudaStream_t st = nullptr;
-    const size_t wb = rh->wbytes;
-    Scratch buf;
-    if (buf.get((size_t)span * 8 + (wb == 4 ? (size_t)span * 4 : 0), st)) return -1;
-    uint64_t* d64 = (uint64_t*)buf.p;
-    CK(cudaMemcpyAsync(d64, x + lo, (size_t)span * 8, cudaMemcpyHostToDevice, st));
-    int rc;
-    int nb = (int)std::min<int64_t>((span + 255) / 256, 148 * 16);
-    if (wb == 4) {
-        uint32_t* dw = (uint32_t*)(d64 + span);
-        k_u64_to_w<uint32_t><<<nb, 256, 0, st>>>(d64, dw, span);
-        rc = rh->kind == 0 ? dispatch_tft<F30>(rh, dw, count, 0, 0, o.data(), len, inverse, st)
-                           : dispatch_tft<F32>(rh, dw, count, 0, 0, o.data(), len, inverse, st);
-        if (rc) return rc;
-        k_w_to_u64<uint32_t><<<nb, 256, 0, st>>>(dw, d64, span);
-        g_launches += 2;
-    } else {
-        rc = dispatch_tft<F62>(rh, d64, count, 0, 0, o.data(), len, inverse, st);
-        if (rc) return rc;
-    }
-    CK(cudaMemcpyAsync(x + lo, d64, (size_t)span * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return 0;
 }
 
 struct tftb_ring {
@@ -468,10 +603,43 @@ int tftb_ring_get(uint64_t p, uint64_t top, int K, tftb_ring** out) {
 
 int tftb_ring_word_bytes(const tftb_ring* ring) { return ring ? ring->h->wbytes : -1; }
 
+}  // extern "C"
+
+namespace {
+// Layout checks of the device batch entry points (tftbt200.h: vectors must
+// not overlap): offsets >= 0, lengths in [1, 2^K], stride >= n.
+int check_layout(const RingHost* rh, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
+                 const int64_t* h_len) {
+    if (count < 0) return fail("negative vector count");
+    const int64_t maxn = rh->K < 62 ? (1ll << rh->K) : INT64_MAX;
+    if (!h_off && !h_len) {
+        if (count > 0 && (n <= 0 || n > maxn)) return fail("vector length outside [1, 2^K]");
+        if (count > 1 && stride < n) return fail("stride shorter than the vector length (vectors overlap)");
+        return 0;
+    }
+    std::vector<std::pair<int64_t, int64_t>> iv(count);
+    for (int64_t v = 0; v < count; v++) {
+        const int64_t o = h_off ? h_off[v] : v * stride;
+        const int64_t l = h_len ? h_len[v] : n;
+        if (l <= 0 || l > maxn) return fail("vector length outside [1, 2^K]");
+        if (o < 0) return fail("negative vector offset");
+        iv[v] = {o, l};
+    }
+    std::sort(iv.begin(), iv.end());
+    for (int64_t v = 1; v < count; v++)
+        if (iv[v].first < iv[v - 1].first + iv[v - 1].second) return fail("vectors overlap");
+    return 0;
+}
+}  // namespace
+
+extern "C" {
+
 int tftb_tft_dev(const tftb_ring* ring, void* data, int64_t count, int64_t n, int64_t stride, const int64_t* h_off,
                  const int64_t* h_len, int inverse, void* stream) {
     if (!ring) return fail("null ring");
     const RingHost* rh = ring->h;
+    if (check_layout(rh, count, n, stride, h_off, h_len)) return -1;
+    if (count > 0 && !data) return fail("null data");
     cudaStream_t st = (cudaStream_t)stream;
     switch (rh->kind) {
         case 0: return dispatch_tft<F30>(rh, data, count, n, stride, h_off, h_len, inverse, st);
@@ -490,11 +658,12 @@ int tftb_plan_create(const tftb_ring* ring, int64_t count, int64_t n, int64_t st
     if (!ring || !out) return fail("null ring / out");
     if (count <= 0) return fail("plan needs at least one vector");
     const RingHost* rh = ring->h;
+    if (check_layout(rh, count, n, stride, h_off, h_len)) return -1;
     std::unique_ptr<tftb_plan> pl(new tftb_plan());
     pl->kind = rh->kind;
-    int rc = rh->kind == 0 ? plan_create<F30>(rh, count, n, stride, h_off, h_len, &pl->impl)
-             : rh->kind == 1 ? plan_create<F32>(rh, count, n, stride, h_off, h_len, &pl->impl)
-                             : plan_create<F62>(rh, count, n, stride, h_off, h_len, &pl->impl);
+    int rc = rh->kind == 0 ? plan_create<F30>(rh, count, n, stride, h_off, h_len, &pl->impl, nullptr, false)
+             : rh->kind == 1 ? plan_create<F32>(rh, count, n, stride, h_off, h_len, &pl->impl, nullptr, false)
+                             : plan_create<F62>(rh, count, n, stride, h_off, h_len, &pl->impl, nullptr, false);
     if (rc) return rc;
     *out = pl.release();
     return 0;
@@ -519,7 +688,10 @@ int tftb_multiply_dev(const tftb_ring* ring, const void* a, int64_t la, int64_t 
                       int64_t sb, void* x, int64_t sx, int64_t count, void* scratch, void* stream) {
     if (!ring) return fail("null ring");
     if (la <= 0 || lb <= 0) return fail("cannot multiply an empty polynomial");
+    if (count < 0) return fail("negative pair count");
+    if (count > 1 && (sa < la || sb < lb)) return fail("operand strides shorter than the operands");
     const RingHost* rh = ring->h;
+    if (rh->K < 62 && la + lb - 1 > (1ll << rh->K)) return fail("product length exceeds 2^K");
     cudaStream_t st = (cudaStream_t)stream;
     switch (rh->kind) {
         case 0: return dispatch_mul<F30>(rh, a, la, sa, b, lb, sb, x, sx, count, scratch, st);

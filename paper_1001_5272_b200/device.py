@@ -16,6 +16,8 @@ import numpy as np
 import torch
 
 from . import backend
+from .modring import UnsupportedSizeError
+from .transforms import DEVICE_MAX_LOG, device_supports
 
 
 def word_dtype(cfg):
@@ -45,8 +47,35 @@ def _stream(stream):
 
 
 def _check_words(t, cfg):
-    if not t.is_cuda or not t.is_contiguous() or t.dtype != word_dtype(cfg):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous() or t.dtype != word_dtype(cfg):
         raise ValueError(f"expected a contiguous CUDA {word_dtype(cfg)} tensor")
+
+
+def _check_lengths(ln, cfg):
+    if (ln <= 0).any() or (ln > (1 << cfg.K)).any():
+        raise ValueError("vector lengths must lie in [1, 2^K]")
+    big = ln[ln > (1 << DEVICE_MAX_LOG)]
+    if big.size and not all(device_supports(int(n)) for n in big):
+        raise UnsupportedSizeError(f"vector lengths beyond the B200 plans' 2^{DEVICE_MAX_LOG} words")
+
+
+def _ragged_layout(lengths, offsets):
+    """Validated (lengths, offsets) int64 arrays: offsets >= 0 and no two
+    vectors overlapping (include/tftb200.h: vectors must not overlap)."""
+    ln = np.ascontiguousarray(lengths, dtype=np.int64).ravel()
+    if offsets is None:
+        of = np.concatenate(([0], np.cumsum(ln)[:-1])).astype(np.int64) if ln.size else ln.copy()
+    else:
+        of = np.ascontiguousarray(offsets, dtype=np.int64).ravel()
+        if of.size != ln.size:
+            raise ValueError("offsets and lengths differ in size")
+        if (of < 0).any():
+            raise ValueError("negative vector offset")
+        order = np.argsort(of, kind="stable")
+        so, sl = of[order], ln[order]
+        if so.size > 1 and (so[1:] < so[:-1] + sl[:-1]).any():
+            raise ValueError("vectors overlap")
+    return ln, of
 
 
 def tft_batch_(data, cfg, n=None, count=1, stride=None, lengths=None, offsets=None, inverse=False,
@@ -59,12 +88,9 @@ def tft_batch_(data, cfg, n=None, count=1, stride=None, lengths=None, offsets=No
     h = backend.ring_handle(cfg)
     lib = backend.load()
     if lengths is not None:
-        ln = np.ascontiguousarray(lengths, dtype=np.int64)
-        of = np.ascontiguousarray(offsets if offsets is not None else np.concatenate(([0], np.cumsum(ln)[:-1])),
-                                  dtype=np.int64)
+        ln, of = _ragged_layout(lengths, offsets)
         count = ln.size
-        if (ln <= 0).any() or (ln > (1 << cfg.K)).any():
-            raise ValueError("vector lengths must lie in [1, 2^K]")
+        _check_lengths(ln, cfg)
         if count and int((of + ln).max()) > data.numel():
             raise ValueError("vectors run past the end of the buffer")
         backend.check(lib.tftb_tft_dev(h, ctypes.c_void_p(data.data_ptr()), count, 0, 0,
@@ -74,8 +100,13 @@ def tft_batch_(data, cfg, n=None, count=1, stride=None, lengths=None, offsets=No
         return data
     if n is None or n <= 0 or n > (1 << cfg.K):
         raise ValueError("n must lie in [1, 2^K]")
+    _check_lengths(np.array([n]), cfg)
+    if count < 0:
+        raise ValueError("negative vector count")
     stride = n if stride is None else stride
-    if (count - 1) * stride + n > data.numel():
+    if count > 1 and stride < n:
+        raise ValueError("stride shorter than the vector length (vectors overlap)")
+    if count and (count - 1) * stride + n > data.numel():
         raise ValueError("vectors run past the end of the buffer")
     backend.check(lib.tftb_tft_dev(h, ctypes.c_void_p(data.data_ptr()), count, n, stride, None, None,
                                    1 if inverse else 0, _stream(stream)))
@@ -87,11 +118,19 @@ def multiply_batch(a, b, x, cfg, count, la, lb, scratch=None, stream=None):
     (a: count*la words, b: count*lb, x: count*(la+lb-1))."""
     for t in (a, b, x):
         _check_words(t, cfg)
+    if count < 0 or la <= 0 or lb <= 0:
+        raise ValueError("need count >= 0 and non-empty operands")
     r = la + lb - 1
     if r > (1 << cfg.K):
-        raise ValueError("product length exceeds 2^K")
+        raise UnsupportedSizeError("product length exceeds 2^K")
+    if not device_supports(r):
+        raise UnsupportedSizeError(f"product length beyond the B200 plans' 2^{DEVICE_MAX_LOG} words")
     if a.numel() < count * la or b.numel() < count * lb or x.numel() < count * r:
         raise ValueError("buffers too small for the batch")
+    if scratch is not None:
+        _check_words(scratch, cfg)
+        if scratch.numel() < count * r:
+            raise ValueError(f"scratch needs count*(la+lb-1) = {count * r} words")
     sp = ctypes.c_void_p(scratch.data_ptr()) if scratch is not None else None
     h = backend.ring_handle(cfg)
     backend.check(backend.load().tftb_multiply_dev(h, ctypes.c_void_p(a.data_ptr()), la, la,
@@ -106,11 +145,10 @@ class BatchPlan:
     execute() issues only kernel launches on the given stream."""
 
     def __init__(self, cfg, lengths, offsets=None):
-        ln = np.ascontiguousarray(lengths, dtype=np.int64)
-        if (ln <= 0).any() or (ln > (1 << cfg.K)).any():
-            raise ValueError("vector lengths must lie in [1, 2^K]")
-        of = np.ascontiguousarray(offsets if offsets is not None else np.concatenate(([0], np.cumsum(ln)[:-1])),
-                                  dtype=np.int64)
+        ln, of = _ragged_layout(lengths, offsets)
+        if ln.size == 0:
+            raise ValueError("a plan needs at least one vector")
+        _check_lengths(ln, cfg)
         self.cfg = cfg
         self.count = int(ln.size)
         self.span = int((of + ln).max()) if ln.size else 0

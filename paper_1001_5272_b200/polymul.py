@@ -20,7 +20,7 @@ from typing import NamedTuple
 
 from . import backend
 from .modring import UnsupportedSizeError
-from .transforms import _credit
+from .transforms import DEVICE_MAX_LOG, _credit, device_supports
 
 
 class BlockStep(NamedTuple):
@@ -48,6 +48,8 @@ def multiply(A, B, X, cfg):
         raise ValueError(f"output buffer has length {len(X)}, need {r}")
     if r > 1 << cfg.K:
         raise UnsupportedSizeError(f"product length {r} exceeds the 2^{cfg.K} roots the config supports")
+    if not device_supports(r):
+        raise UnsupportedSizeError(f"product length {r} exceeds the B200 plans' 2^{DEVICE_MAX_LOG} words")
     if X is A or X is B:
         raise ValueError("output buffer must be distinct from the inputs")
     K = backend.kernels()

@@ -21,11 +21,27 @@ from . import backend
 from .modring import UnsupportedSizeError
 
 
+# Longest transform the device plans cover: two passes over 2^14-word tiles
+# reach 2^28 words (host.h make_plan), and n = 2^28 + r, r <= 4, runs as the
+# 2^28 transform plus r dot products (p2r.cuh).  Rings with K > 28
+# (3221225473: K = 30; the 62-bit prime: K = 57) accept longer lengths in
+# the reference; here they raise UnsupportedSizeError, the reference's own
+# exception for lengths a config cannot transform (transforms.py:28-34).
+DEVICE_MAX_LOG = 28
+DEVICE_P2R_MAX = 4
+
+
+def device_supports(n):
+    return n <= (1 << DEVICE_MAX_LOG) or n - (1 << DEVICE_MAX_LOG) <= DEVICE_P2R_MAX
+
+
 def _check_size(n, cfg):
     if n == 0:
         raise ValueError("cannot transform an empty buffer")
     if n > 1 << cfg.K:
         raise UnsupportedSizeError(f"length {n} exceeds the 2^{cfg.K} roots the config supports")
+    if not device_supports(n):
+        raise UnsupportedSizeError(f"length {n} exceeds the B200 plans' 2^{DEVICE_MAX_LOG}(+{DEVICE_P2R_MAX}) words")
 
 
 def _credit(cfg, mults, adds):

@@ -420,3 +420,79 @@ def test_concurrent_calls_on_distinct_buffers():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.gpu
+def test_layout_validation_rejects_bad_batches():
+    """Negative offsets, overlapping vectors, short strides and short
+    scratch are rejected before any launch (Python wrapper and C ABI)."""
+    import ctypes
+    cfg = T.default_config()
+    d = torch.zeros(1000, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        device.tft_batch_(d, cfg, lengths=[10, 10], offsets=[-1, 20])
+    with pytest.raises(ValueError):
+        device.tft_batch_(d, cfg, lengths=[10, 10], offsets=[0, 5])
+    with pytest.raises(ValueError):
+        device.tft_batch_(d, cfg, n=10, count=3, stride=5)
+    with pytest.raises(ValueError):
+        device.BatchPlan(cfg, [10, 10], [30, 25])
+    a = torch.zeros(20, dtype=torch.int32, device="cuda")
+    x = torch.zeros(39, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        device.multiply_batch(a, a, x, cfg, 1, 20, 20, scratch=torch.zeros(5, dtype=torch.int32, device="cuda"))
+    # the C ABI itself
+    lib = backend.load()
+    h = backend.ring_handle(cfg)
+    off = np.array([0, 5], dtype=np.int64)
+    ln = np.array([10, 10], dtype=np.int64)
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    rc = lib.tftb_tft_dev(h, ctypes.c_void_p(d.data_ptr()), 2, 0, 0, off.ctypes.data_as(p64),
+                          ln.ctypes.data_as(p64), 0, None)
+    assert rc != 0 and b"overlap" in lib.tftb_last_error()
+    off = np.array([-3, 50], dtype=np.int64)
+    rc = lib.tftb_tft_dev(h, ctypes.c_void_p(d.data_ptr()), 2, 0, 0, off.ctypes.data_as(p64),
+                          ln.ctypes.data_as(p64), 0, None)
+    assert rc != 0
+    rc = lib.tftb_tft_dev(h, ctypes.c_void_p(d.data_ptr()), 3, 10, 5, None, None, 0, None)
+    assert rc != 0
+
+
+@pytest.mark.gpu
+def test_host_batch_with_gaps_and_unsorted_offsets():
+    """tftb_tft_batch_u64 transforms only the [off, off+len) runs: words in
+    the gaps (even ones >= 2^32, which no u32 ring word can hold) come back
+    untouched; unsorted offsets work; overlapping ones are rejected."""
+    import ctypes
+    cfg = T.default_config()
+    rng = np.random.default_rng(5)
+    lens = np.array([700, 40000, 1, 9000, 70001, 33], dtype=np.int64)
+    gaps = np.array([3, 0, 17, 1, 5, 2], dtype=np.int64)
+    offs = np.zeros_like(lens)
+    pos = 0
+    for i in range(lens.size):
+        pos += gaps[i]
+        offs[i] = pos
+        pos += lens[i]
+    buf = np.full(pos + 7, (1 << 40) + 12345, dtype=np.uint64)
+    for o, n in zip(offs, lens):
+        buf[o:o + n] = rng.integers(0, cfg.p, n, dtype=np.uint64)
+    orig = buf.copy()
+    perm = np.array([3, 0, 5, 1, 4, 2])
+    lib = backend.load()
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    o2, l2 = offs[perm].copy(), lens[perm].copy()
+    backend.check(lib.tftb_tft_batch_u64(buf.ctypes.data, o2.ctypes.data_as(p64), l2.ctypes.data_as(p64),
+                                         lens.size, cfg.p, cfg.omegaK, cfg.K, 0))
+    mask = np.ones(buf.size, dtype=bool)
+    for o, n in zip(offs, lens):
+        mask[o:o + n] = False
+        assert np.array_equal(buf[o:o + n], O.tft(orig[o:o + n], cfg.p, cfg.omegaK, cfg.K)), n
+    assert np.array_equal(buf[mask], orig[mask])
+    backend.check(lib.tftb_tft_batch_u64(buf.ctypes.data, o2.ctypes.data_as(p64), l2.ctypes.data_as(p64),
+                                         lens.size, cfg.p, cfg.omegaK, cfg.K, 1))
+    assert np.array_equal(buf, orig)
+    bad = np.array([0, 500], dtype=np.int64)
+    rc = lib.tftb_tft_batch_u64(buf.ctypes.data, bad.ctypes.data_as(p64), lens[:2].copy().ctypes.data_as(p64),
+                                2, cfg.p, cfg.omegaK, cfg.K, 0)
+    assert rc != 0 and b"overlap" in lib.tftb_last_error()

@@ -115,3 +115,31 @@ def test_no_cpu_fallback_env(tmp_path):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        cwd=str(__import__("pathlib").Path(__file__).parent.parent))
     assert r.returncode != 0 and "no CPU path" in r.stderr
+
+
+class _Len:
+    """A buffer stand-in with only a length: the size checks run before
+    anything touches the words."""
+
+    def __init__(self, n):
+        self.n = n
+
+    def __len__(self):
+        return self.n
+
+
+def test_lengths_beyond_the_device_plans_raise_unsupported():
+    """Lengths the reference's ring accepts (K = 30 for 3221225473) but the
+    device plans do not cover (> 2^28 + 4) raise the reference's
+    UnsupportedSizeError before any dispatch."""
+    c = T.config_for_modulus(3221225473)
+    for n in ((1 << 28) + 5, (1 << 29) + 1, 1 << 30):
+        with pytest.raises(UnsupportedSizeError):
+            T.tft(_Len(n), c)
+        with pytest.raises(UnsupportedSizeError):
+            T.itft(_Len(n), c)
+    with pytest.raises(UnsupportedSizeError):
+        T.multiply(_Len(1 << 27), _Len((1 << 27) + 100), _Len((1 << 28) + 99), c)
+    from paper_1001_5272_b200.transforms import device_supports
+    assert device_supports(1 << 28) and device_supports((1 << 28) + 4)
+    assert not device_supports((1 << 28) + 5)

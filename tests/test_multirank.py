@@ -65,3 +65,44 @@ def test_gather_two_ranks_gloo():
     for r, (s, e) in enumerate(ranges):
         want += [r + 1] * int(sum(lens[s:e]))
     assert out == want
+
+
+def _worker_transform(rank, world, port, q):
+    """Each rank transforms its shard of one ragged batch (the CPU oracle
+    stands in for the rank's GPU), then the results are gathered to rank 0
+    -- the bench's sharded config-2 path at reduced size."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p, top, K = 998244353, pow(3, 119, 998244353), 23
+    rng = np.random.default_rng(1)
+    lens = rng.integers(1, 3000, 37).astype(np.int64)
+    flat = rng.integers(0, p, int(lens.sum()), dtype=np.uint64)
+    s, e, ln, off = local_shard(lens, rank, world)
+    base = int(np.concatenate(([0], np.cumsum(lens)))[s])
+    mine = flat[base:base + int(ln.sum())]
+    out = O.tft_batch(mine, ln, p, top, K)
+    local = torch.from_numpy(out.astype(np.int64))
+    full = gather_to_root(local)
+    if rank == 0:
+        want = O.tft_batch(flat, lens, p, top, K).astype(np.int64)
+        q.put(bool(np.array_equal(full.numpy(), want)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_transform_and_gather_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_transform, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert ok

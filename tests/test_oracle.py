@@ -91,3 +91,24 @@ def test_reference_kernels_agree_when_built(primes):
         buf = array("Q", x.tobytes())
         ref.tft(memoryview(buf), 0, n, p, top, K)
         assert np.array_equal(np.frombuffer(buf.tobytes(), dtype=np.uint64), O.tft(x, p, top, K))
+
+
+def test_oracle_matches_reference_config5_digests():
+    """The oracle against the reference's digests of config 5's pinned
+    inputs (tests/golden/configs.json), the lengths it finishes quickly."""
+    import json
+    import os
+    import workloads as W
+    from conftest import sha
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs.json")) as f:
+        cg = json.load(f)
+    done = 0
+    for rec in cg["config5"]:
+        if rec["n"] > 20000:
+            continue
+        p, top, K = cg["rings"][str(rec["p"])]
+        x = W.c5(rec["n"], rec["leg"], 1)
+        assert sha(O.tft(x, p, top, K)) == rec["tft"][0], (rec["leg"], rec["n"])
+        assert sha(O.itft(x, p, top, K)) == rec["itft"][0], (rec["leg"], rec["n"])
+        done += 1
+    assert done >= 30

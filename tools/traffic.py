@@ -35,6 +35,7 @@ out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram
                     for d in ours]}
 tot = lambda ds: sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds)
 inv = [d for d in ours if "k_cli_" in d["kernel"]]
+out["forward_bytes"] = tot([d for d in ours if "k_clg_fwd" in d["kernel"]])
 out["config2_bytes_per_step"] = tot(ours)
 out["config2_read_bytes"] = sum(d["dram__bytes_read.sum"] for d in ours)
 out["config2_write_bytes"] = sum(d["dram__bytes_write.sum"] for d in ours)
