@@ -338,14 +338,22 @@ def main():
     import paper_1001_5272_b200 as T
     from paper_1001_5272_b200 import backend, device, shard
 
-    torch.cuda.set_device(local)
+    # (BENCH_DIST_BACKEND=gloo: a functional smoke of the multi-rank plumbing
+    # on a one-GPU box -- ranks share the device, the gather goes through
+    # host memory; never a measurement)
+    dist_backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    local = local % max(1, torch.cuda.device_count())
     if args.config != 2:
         explore(args, T, device, backend, torch)
         return
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(dist_backend)
     cfg = T.default_config()
     g = golden()
     lens_all, flat_all = W.c2(1)
@@ -374,7 +382,7 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         t_g0.record(stream)
-        full = shard.gather_to_root(d, root=0)
+        full = shard.gather_to_root(d if dist_backend == "nccl" else d.cpu(), root=0)
         t_g1.record(stream)
         torch.cuda.synchronize()
         gather_ms = t_g0.elapsed_time(t_g1)
@@ -457,14 +465,14 @@ def main():
     def allmax(v):
         if not dist:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}" if dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def allsum(v):
         if not dist:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}" if dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 

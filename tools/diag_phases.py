@@ -17,7 +17,7 @@ for inv in [2]:  # forward only (the split inverse has no phase stamps)
         d = torch.randint(0, cfg.p, (cnt * n,), dtype=torch.int32, device="cuda")
         t = torch.zeros(cnt * G * 8, dtype=torch.int64, device="cuda")
         for _ in range(2):
-            backend.check(f(cfg.p, cfg.omegaK, cfg.K, d.data_ptr(), n, cnt, t.data_ptr(), inv))
+            backend.check(f(cfg.p, cfg.omegaK, cfg.K, d.data_ptr(), n, cnt, t.data_ptr(), 0 if inv == 2 else inv))
         a = t.cpu().numpy().reshape(-1, 8).astype(np.float64)
         last = 7 if inv == 1 else 6
         if inv == 1 and n % 16384 == 0:
