@@ -280,6 +280,48 @@ def config3_record(args, T, device, torch, peak, g):
             "fwd_frac_min": min(o["fwd_frac"] for o in out), "inv_frac_min": min(o["inv_frac"] for o in out)}
 
 
+def config4_record(args, T, device, torch, peak, g):
+    """Config 4: 256 products 2,500,001 x 1,750,004 (seed 3) in one batched
+    multiply (three transforms + fused pointwise product per pair).  Pairs
+    0 and 255 are checked against the reference's digests before timing."""
+    cfg = T.default_config()
+    la, lb, pairs = W.C4_LA, W.C4_LB, W.C4_PAIRS
+    r = la + lb - 1
+    wd = device.word_dtype(cfg)
+    a = torch.empty(pairs * la, dtype=wd, device="cuda")
+    b = torch.empty(pairs * lb, dtype=wd, device="cuda")
+    for k, pa, pb in W.c4_pairs(range(pairs)):  # one pair at a time: small host footprint
+        a[k * la:(k + 1) * la] = device.to_words(pa, cfg)
+        b[k * lb:(k + 1) * lb] = device.to_words(pb, cfg)
+    x = torch.empty(pairs * r, dtype=wd, device="cuda")
+    y = torch.empty(pairs * r, dtype=wd, device="cuda")
+    device.multiply_batch(a, b, x, cfg, pairs, la, lb, scratch=y)
+    refs = {rec["pair"]: rec["x"] for rec in (g or {}).get("config4", [])}
+    parity = {}
+    for k in (0, 255):
+        if k in refs:
+            parity[k] = sha_words(device.from_words(x[k * r:(k + 1) * r], cfg)) == refs[k]
+            if not parity[k]:
+                raise SystemExit(f"config 4 parity failure at pair {k}")
+    for _ in range(args.warmup):
+        device.multiply_batch(a, b, x, cfg, pairs, la, lb, scratch=y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        device.multiply_batch(a, b, x, cfg, pairs, la, lb, scratch=y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    byt = pairs * (4 * (la + lb) + 3 * (2 * passes_min(r) * r * 4) + 3 * r * 4)
+    del a, b, x, y
+    torch.cuda.empty_cache()
+    return {"pairs": pairs, "la": la, "lb": lb, "seed": 3, "ms_per_batch": ms, "products_per_s": pairs / ms * 1e3,
+            "roofline_frac": byt / (ms / 1e3) / 1e9 / peak,
+            "algorithmic_bytes": "per pair 4(la+lb) + 3*2*2*r*4 + 3*r*4 (SURVEY.md §8(d) 3-transform convention)",
+            "parity_sha256_pairs_0_255": parity, "l2": "inputs 4.4 GB > L2; no flush"}
+
+
 def percall_e2e(T, lens, flat):
     """The reference arm's call pattern through the drop-in: one
     `_kernels.tft` call per vector on an array('Q') buffer, from a thread
@@ -542,7 +584,7 @@ def main():
                          "note": "algorithmic bytes 2*passes_min(n)*n*4 per vector per direction "
                                  "(BASELINE.md §5) over the pass's CUDA-event time; traffic = ncu "
                                  "dram read+write of the same launches (profiles/traffic.json)"},
-            "roofline_inverse": {"bound": "hbm", "kernel": "inverse pass (k_cli_chunks + k_cli_cols)",
+            "roofline_inverse": {"bound": "hbm", "kernel": "inverse pass (k_cli_chunks; the last chunk CTA of each vector solves its columns)",
                                  "achieved": inv_ach, "peak": peak, "unit": "GB/s", "frac": inv_ach / peak,
                                  "traffic": traffic.get("inverse_pass_bytes")},
             "roofline_step": {"achieved": step_ach, "frac": step_ach / peak,
@@ -564,6 +606,7 @@ def main():
                 line["e2e_percall"] = percall_e2e(T, lens_all, flat_all)
             if not args.no_c3:
                 line["config3"] = config3_record(args, T, device, torch, peak, g)
+                line["config4"] = config4_record(args, T, device, torch, peak, g)
             if not args.no_cpu:
                 line["cpu_baseline"] = cpu_reference(lens_all, flat_all)
         print(json.dumps(line))

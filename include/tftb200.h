@@ -57,6 +57,18 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
 int tftb_tft_batch_u64(uint64_t* x, const int64_t* off, const int64_t* len, int64_t count,
                        uint64_t p, uint64_t top, int K, int inverse);
 
+/* Replaces `polymul.horner_eval(poly, point, cfg)` (reference polymul.py:39-52;
+ * its compiled twin `horner_k`, _kernels.pyx:401-412): *out = sum_i poly[i]
+ * point^i mod p over n >= 1 canonical host words, evaluated on the device
+ * (segment Horner per thread, block reduction). */
+int tftb_horner_u64(const uint64_t* poly, int64_t n, uint64_t point, uint64_t p, uint64_t* out);
+
+/* Replaces `polymul.fold_twist(src, X, base, L, q, cfg)` (reference
+ * polymul.py:55-88; `fold_twist_k`, _kernels.pyx:366-398): X[i mod L] +=
+ * src[i] w^i for i < ls (X = the host block X + base, L words, w = omega(q);
+ * w = 1 for q = 0), on the device. */
+int tftb_fold_twist_u64(const uint64_t* src, int64_t ls, uint64_t* X, int64_t L, uint64_t w, uint64_t p);
+
 /* ---------------------------------------------------------------- rings */
 typedef struct tftb_ring tftb_ring;
 

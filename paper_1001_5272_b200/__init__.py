@@ -30,7 +30,7 @@ from .modring import (
     root_of_level,
     zeros,
 )
-from .polymul import BlockStep, block_schedule, multiply
+from .polymul import BlockStep, block_schedule, fold_twist, horner_eval, multiply
 from .transforms import fft_pow2, itft, tft
 
 __version__ = "0.1.0"
@@ -38,7 +38,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BlockStep", "OpCounters", "RingConfig", "RingConfigError", "UnsupportedSizeError",
     "backend_name", "block_schedule", "ceil_lg", "config_for_modulus", "default_config",
-    "fft_pow2", "is_probable_prime", "itft", "kernel_view", "kernels", "make_buffer",
+    "fft_pow2", "fold_twist", "horner_eval", "is_probable_prime", "itft", "kernel_view", "kernels", "make_buffer",
     "multiply", "omega", "revbin", "revbin_increment", "ring_add", "ring_mul", "ring_pow",
     "ring_sub", "root_of_level", "tft", "zeros", "__version__",
 ]

@@ -45,6 +45,9 @@ SIGNATURES = {
                                          ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, _i64p, _i64p]),
     "tftb_tft_batch_u64": (ctypes.c_int, [_vp, _i64p, _i64p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64,
                                           ctypes.c_int, ctypes.c_int]),
+    "tftb_horner_u64": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _u64p]),
+    "tftb_fold_twist_u64": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_uint64,
+                                           ctypes.c_uint64]),
     "tftb_ring_get": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_vp)]),
     "tftb_ring_word_bytes": (ctypes.c_int, [_vp]),
     "tftb_tft_dev": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, _i64p,

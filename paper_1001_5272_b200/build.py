@@ -10,7 +10,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-UNITS = ["tftb200.cu", "inst_f30.cu", "inst_f32.cu", "inst_f62.cu", "debug.cu"]
+UNITS = ["tftb200.cu", "inst_f30.cu", "inst_f32.cu", "inst_f62.cu", "debug.cu", "poly.cu"]
 OUT = os.path.join(HERE, "libtftb200.so")
 STAMP = OUT + ".stamp"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

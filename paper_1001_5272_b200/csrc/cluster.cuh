@@ -507,6 +507,57 @@ TFT_DEV void colq_solve(const F& f, typename F::W* x, typename F::W* S, uint32_t
 // Every CTA works alone, so nothing waits on a sibling; the price is one
 // more read and write of the vector (the in-between state stays in the
 // n-word buffer: no scratch).
+// B: the column solves and the last chunk's phases 2/3 of vector v (rows
+// read through L2: in the fused launch they were written moments ago)
+template <class F, int CL>
+TFT_DEV void cli_cols_body(const LaunchArgs<F>& a, int64_t v, typename F::W* S, bool prefetch) {
+    using W = typename F::W;
+    constexpr uint32_t C = 1u << CL;
+    const int64_t n = a.xd.n(v);
+    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
+    W* x = a.x + a.xd.o(v);
+    const F f = a.f;
+    // stream the vector into L2 (TMA bulk prefetch) while the first quads load
+    if (prefetch && threadIdx.x == 0) l2_prefetch(x, n);
+    const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
+    const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
+    switch (K) {  // columns >= h: K rows
+#define TFTB_C1(k)                                                                          \
+    case k:                                                                                 \
+        if (h) colq_solve<F, k, false, true>(f, x, S, C, h, C, b1, b1M);                    \
+        else colq_solve<F, k, false, false>(f, x, S, C, 0, C, b1, b1M);                     \
+        break;
+        TFTB_C1(1) TFTB_C1(2) TFTB_C1(3) TFTB_C1(4) TFTB_C1(5) TFTB_C1(6) TFTB_C1(7)
+        default: colq_solve<F, 8, false, false>(f, x, S, C, 0, C, b1, b1M); break;  // K = 8: h = 0
+#undef TFTB_C1
+    }
+    TFTB_STAMP(a, 4);
+    if (!h) return;
+    // the last chunk's known outputs [0, h) (its tail [h, C) came from the
+    // column solve above: no zero fill)
+    tile_load<W>(S, x + (size_t)K * C, h, h, [](uint32_t, W w) { return w; });
+    __syncthreads();
+    TFTB_STAMP(a, 5);
+    const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
+    itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
+    TFTB_STAMP(a, 6);
+    const Tw<W>* b2 = a.R.vinvT + 72 * K;
+    const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
+    switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
+#define TFTB_C2(m)                                                                          \
+    case m: colq_solve<F, m, true, false>(f, x, S, C, 0, h, b2, b2M); break;
+        TFTB_C2(2) TFTB_C2(3) TFTB_C2(4) TFTB_C2(5) TFTB_C2(6) TFTB_C2(7) TFTB_C2(8)
+#undef TFTB_C2
+    }
+}
+
+// A (and, fused, B): chunk g of vector v runs its inverse rounds and stores
+// the tile back.  With a.done (the production path) the vector's chunk CTAs
+// then take a ticket, and the LAST one to finish runs B for the vector
+// right away: no second launch, no CTA ever waits on a sibling, and the
+// rows B reads were written microseconds earlier, so they come from L2
+// (and the first, intermediate write of each row is usually overwritten
+// there before it reaches HBM).  Tickets are self-resetting.
 template <class F, int CL>
 __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F> a) {
     using W = typename F::W;
@@ -522,15 +573,39 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F
     const int64_t o = a.xd.o(v);
     W* x = a.x + o;
     const F f = a.f;
+    TFTB_STAMP(a, 0);
     if (a.pre)
         tile_load_pre<F>(a, S, x + cbase, a.pre + o + cbase, n - cbase, C);
     else
         tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
+    TFTB_STAMP(a, 1);
     const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
     if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
-    tile_store<W>(x + cbase, S, (uint32_t)min((int64_t)C, n - cbase), [](W w) { return w; });
+    TFTB_STAMP(a, 2);
+    const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
+    if (!a.done) {
+        tile_store<W>(x + cbase, S, lim, [](W w) { return w; });
+        return;
+    }
+    const auto id = [](W w) { return w; };
+    tile_store<W, decltype(id), false>(x + cbase, S, lim, id);
+    __shared__ unsigned last;
+    __threadfence();  // this CTA's rows, visible device-wide before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned chunks = K + (h ? 1u : 0u);
+        const unsigned t = atomicAdd(a.done + (v - a.vbase), 1u);
+        last = t == chunks - 1;
+        if (last) a.done[v - a.vbase] = 0;  // reset for the next execution
+    }
+    __syncthreads();
+    TFTB_STAMP(a, 3);
+    if (!last) return;
+    __threadfence();  // acquire: the siblings' rows
+    cli_cols_body<F, CL>(a, v, S, false);
+    TFTB_STAMP(a, 7);
 }
 
 template <class F, int CL>
@@ -538,41 +613,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_cols(LaunchArgs<F> 
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     W* S = reinterpret_cast<W*>(smem_raw);
-    constexpr uint32_t C = 1u << CL;
-    const int64_t v = a.vbase + blockIdx.x;
-    const int64_t n = a.xd.n(v);
-    const uint32_t K = (uint32_t)(n >> CL), h = (uint32_t)(n & (C - 1));
-    W* x = a.x + a.xd.o(v);
-    const F f = a.f;
-    // stream the vector into L2 (TMA bulk prefetch) while the first quads load
-    if (threadIdx.x == 0) l2_prefetch(x, n);
-    const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
-    const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
-    switch (K) {  // columns >= h: K rows
-#define TFTB_C1(k)                                                                          \
-    case k:                                                                                 \
-        if (h) colq_solve<F, k, false, true>(f, x, S, C, h, C, b1, b1M);                    \
-        else colq_solve<F, k, false, false>(f, x, S, C, 0, C, b1, b1M);                     \
-        break;
-        TFTB_C1(1) TFTB_C1(2) TFTB_C1(3) TFTB_C1(4) TFTB_C1(5) TFTB_C1(6) TFTB_C1(7)
-        default: colq_solve<F, 8, false, false>(f, x, S, C, 0, C, b1, b1M); break;  // K = 8: h = 0
-#undef TFTB_C1
-    }
-    if (!h) return;
-    // the last chunk's known outputs [0, h) (its tail [h, C) came from the
-    // column solve above: no zero fill)
-    tile_load<W>(S, x + (size_t)K * C, h, h, [](uint32_t, W w) { return w; });
-    __syncthreads();
-    const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
-    itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
-    const Tw<W>* b2 = a.R.vinvT + 72 * K;
-    const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
-    switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
-#define TFTB_C2(m)                                                                          \
-    case m: colq_solve<F, m, true, false>(f, x, S, C, 0, h, b2, b2M); break;
-        TFTB_C2(2) TFTB_C2(3) TFTB_C2(4) TFTB_C2(5) TFTB_C2(6) TFTB_C2(7) TFTB_C2(8)
-#undef TFTB_C2
-    }
+    cli_cols_body<F, CL>(a, a.vbase + blockIdx.x, S, true);
 }
 
 // ================================================ two-pass plan, chunk pass
@@ -934,11 +975,18 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
     const uint32_t nq = (C - head) / NV;
     const W* base = in + head;
     constexpr int UNR = GP <= 4 ? 2 : 1;
+    // The vector's G CTAs start together and read the same rows.  Each
+    // starts at its own 1/GP of the columns (rotated order), so at any
+    // moment they fetch different lines: one CTA brings a line from HBM and
+    // the siblings that reach it later hit it in L2, instead of all G
+    // waiting on the same HBM fill in lockstep.
+    const uint32_t shift = GI * (nq / GP);
+    auto rot = [&](uint32_t q) { return q >= nq ? q : (q + shift < nq ? q + shift : q + shift - nq); };
     for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += blockDim.x * UNR) {
         typename V::T buf[UNR][GP];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const uint32_t o = (q0 + u * blockDim.x) * NV;
+            const uint32_t o = rot(q0 + u * blockDim.x) * NV;
 #pragma unroll
             for (int j = 0; j < GP; ++j) {
                 const W* src = base + (size_t)j * C + o;
@@ -959,7 +1007,7 @@ TFT_DEV void cone_fill(const F& f, typename F::W* S, const typename F::W* in, in
         for (int u = 0; u < UNR; ++u) {
             const uint32_t q = q0 + u * blockDim.x;
             if (q >= nq) break;
-            const uint32_t i0 = head + q * NV;
+            const uint32_t i0 = head + rot(q) * NV;
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 W vals[GP];

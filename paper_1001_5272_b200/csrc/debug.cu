@@ -49,7 +49,6 @@ extern "C" int tftb_debug_intt_tile(uint64_t p, uint64_t top, int K, void* data,
 extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* data, int64_t n, int64_t count,
                                          unsigned long long* out, int inverse) {
     using namespace tftb;
-    if (inverse) return fail("debug: the split inverse has no phase stamps (time its two launches instead)");
     RingHost* rh;
     if (get_ring(p, top, K, &rh)) return -1;
     if (rh->kind != 0) return fail("debug: F30 only");
@@ -65,6 +64,16 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     a.timing = out;
     constexpr int CL = Limits<F30>::CL;
     const size_t smem = padded_words(1u << CL) * 4;
+    if (inverse) {  // the fused split inverse: chunk phases, and the last CTA's column work
+        if (set_smem(k_cli_chunks<F30, CL>, smem)) return -1;
+        Scratch tickets;
+        if (tickets.get((size_t)count * 4, nullptr)) return -1;
+        CK(cudaMemset(tickets.p, 0, (size_t)count * 4));
+        a.done = (unsigned*)tickets.p;
+        k_cli_chunks<F30, CL><<<dim3(pl.G, (unsigned)count), 256, smem>>>(a);
+        CK(cudaDeviceSynchronize());
+        return 0;
+    }
     const int gam = pl.l - CL;
     void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
                                  : gam == 2 ? (pl.G == 3 ? k_clg_fwd<F30, CL, 2, 3> : k_clg_fwd<F30, CL, 2>)

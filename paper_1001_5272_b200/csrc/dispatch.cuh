@@ -153,10 +153,24 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
         if (inverse ? (set_smem(k_cli_chunks<F, CL>, smem) || set_smem(k_cli_cols<F, CL>, smem))
                     : fsplit ? (set_smem(kf, smem) || set_smem(k_clf_chunks<F, CL>, smem)) : set_smem(kg, smem))
             return -1;
+        // fused split inverse: per-vector chunk tickets (zeroed once here,
+        // self-resetting in the kernel); TFTB_SPLIT_INV=1 keeps the two launches
+        static const bool two_launch = getenv("TFTB_SPLIT_INV") != nullptr;
+        Scratch tickets;
+        if (inverse && !two_launch) {
+            const size_t tb = (size_t)std::min<int64_t>(count, 65535) * sizeof(unsigned);
+            if (tickets.get(tb, st)) return -1;
+            CK(cudaMemsetAsync(tickets.p, 0, tb, st));
+            a.done = (unsigned*)tickets.p;
+        }
         for (int64_t v0 = 0; v0 < count; v0 += 65535) {
             a.vbase = v0;
             unsigned nv = (unsigned)std::min<int64_t>(count - v0, 65535);
-            if (inverse) {
+            if (inverse && !two_launch) {
+                k_cli_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
+                CK(cudaGetLastError());
+                g_launches += 1;
+            } else if (inverse) {
                 // split inverse: per-chunk launch, then one CTA per vector
                 k_cli_chunks<F, CL><<<dim3(pl.G, nv, 1), kNT, smem, st>>>(a);
                 CK(cudaGetLastError());

@@ -49,6 +49,7 @@ struct LaunchArgs {
     int l0, l1, wlog;     // two-pass plan (large kernels)
     int64_t vbase;        // first vector of this launch
     unsigned long long* timing;  // debug: per-CTA phase timestamps (null in production)
+    unsigned* done;              // per-vector chunk tickets (fused split inverse), v - vbase
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -198,7 +199,7 @@ TFT_DEV void tile_load_pre(const LaunchArgs<F>& a, typename F::W* S, const typen
 }
 
 // dst[i] = cv(S[phys(i)]) for i < lim, 16-byte stores for the aligned body
-template <typename W, class CV>
+template <typename W, class CV, bool STREAM = true>
 TFT_DEV void tile_store(W* dst, const W* S, uint32_t lim, const CV& cv, Lanes ln = cta_lanes()) {
     using V = Vec16<W>;
     constexpr int NV = V::N;
@@ -212,7 +213,8 @@ TFT_DEV void tile_store(W* dst, const W* S, uint32_t lim, const CV& cv, Lanes ln
         W e[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) e[q] = cv(S[(i + q) + ((i + q) >> 5)]);
-        __stcs(vd + k, V::make(e));
+        if constexpr (STREAM) __stcs(vd + k, V::make(e));
+        else __stcg(vd + k, V::make(e));  // re-read soon from L2
     }
     for (uint32_t i = head + nq * NV + ln.id; i < lim; i += ln.n) dst[i] = cv(S[i + (i >> 5)]);
 }

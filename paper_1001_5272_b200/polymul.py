@@ -12,7 +12,9 @@ formulation BASELINE config 4 describes.  Because the arithmetic is exact
 the coefficients are identical to the reference's Algorithm 3 (its
 pre-inverse state is the same DFT, reference tests/test_polymul.py:143-168).
 block_schedule is the reference's greedy power-of-two cover (polymul.py:25-36),
-kept for API parity; the device does not need it.
+kept for API parity; the device does not need it.  horner_eval and
+fold_twist, the reference's Algorithm-3 helpers (polymul.py:39-88), run on
+the device too (csrc/poly.cu), so the module's whole public surface is GPU.
 """
 
 from array import array
@@ -20,6 +22,7 @@ from typing import NamedTuple
 
 from . import backend
 from .modring import UnsupportedSizeError
+from .modring import omega
 from .transforms import DEVICE_MAX_LOG, _credit, device_supports
 
 
@@ -36,6 +39,55 @@ def block_schedule(r):
         ell = (r - q).bit_length() - 2
         yield BlockStep(q, ell, 1 << ell)
         q += 1 << ell
+
+
+def _words(buf):
+    """(address, keepalive) of a buffer's uint64 words, staged when the
+    kernels cannot view it in place."""
+    import numpy as np
+    mv = backend.kernel_view(buf, writable=False)
+    if mv is None:
+        mv = memoryview(array("Q", buf))
+    return (np.frombuffer(mv, dtype=np.uint64).ctypes.data if len(mv) else None), mv
+
+
+def horner_eval(poly, point, cfg):
+    """Evaluate a nonempty coefficient sequence at one ring point (reference
+    polymul.py:39-52), on the GPU."""
+    import ctypes
+    if len(poly) == 0:
+        raise ValueError("cannot evaluate an empty polynomial")
+    addr, keep = _words(poly)
+    out = ctypes.c_uint64(0)
+    backend.check(backend.load().tftb_horner_u64(addr, len(keep), point % cfg.p, cfg.p, ctypes.byref(out)))
+    n = len(poly) - 1
+    _credit(cfg, n, n)
+    return int(out.value)
+
+
+def fold_twist(src, X, base, L, q, cfg):
+    """Accumulate the twisted fold of src into the block X[base : base+L]
+    (reference polymul.py:55-88): block slot i gains the sum of
+    src[i + j*L] * omega(q)^(i + j*L) over j, on the GPU."""
+    if L <= 0 or base < 0 or base + L > len(X):
+        raise IndexError("fold block outside the output buffer")
+    s_addr, s_keep = _words(src)
+    w = omega(q, cfg) if q else 1
+    mvx = backend.kernel_view(X)
+    staged = None
+    if mvx is None:
+        staged = array("Q", X[base:base + L])
+        mvx, off = memoryview(staged), 0
+    else:
+        off = base
+    import numpy as np
+    x_addr = np.frombuffer(mvx, dtype=np.uint64).ctypes.data + 8 * off
+    backend.check(backend.load().tftb_fold_twist_u64(s_addr, len(s_keep), x_addr, L, w, cfg.p))
+    if staged is not None:
+        for i, v in enumerate(staged):
+            X[base + i] = v
+    ls = len(src)
+    _credit(cfg, 2 * (ls - 1) if q and ls else 0, ls)
 
 
 def multiply(A, B, X, cfg):
