@@ -633,6 +633,8 @@ def explore(args, T, device, backend, torch):
     on the pinned inputs of workloads.py."""
     peak, _ = peaks()
     out = []
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     if args.config == 1:
         cfg = T.default_config()
         x = W.c1()
@@ -673,6 +675,7 @@ def explore(args, T, device, backend, torch):
             print(json.dumps(out[-1]), flush=True)
             del d, plan
             torch.cuda.empty_cache()
+        print(json.dumps({"config": args.config, "clocks": clocks.stop()}))
         return
     elif args.config == 4:
         cfg = T.default_config()
@@ -690,6 +693,7 @@ def explore(args, T, device, backend, torch):
                     "roofline_frac": byt / (t / 1e3) / 1e9 / peak})
     for o in out:
         print(json.dumps(o))
+    print(json.dumps({"config": args.config, "clocks": clocks.stop()}))
 
 
 if __name__ == "__main__":

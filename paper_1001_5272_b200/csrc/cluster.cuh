@@ -531,16 +531,13 @@ TFT_DEV void cli_cols_body(const LaunchArgs<F>& a, int64_t v, typename F::W* S, 
         default: colq_solve<F, 8, false, false>(f, x, S, C, 0, C, b1, b1M); break;  // K = 8: h = 0
 #undef TFTB_C1
     }
-    TFTB_STAMP(a, 4);
     if (!h) return;
     // the last chunk's known outputs [0, h) (its tail [h, C) came from the
     // column solve above: no zero fill)
     tile_load<W>(S, x + (size_t)K * C, h, h, [](uint32_t, W w) { return w; });
     __syncthreads();
-    TFTB_STAMP(a, 5);
     const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
     itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
-    TFTB_STAMP(a, 6);
     const Tw<W>* b2 = a.R.vinvT + 72 * K;
     const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
     switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
@@ -573,17 +570,14 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F
     const int64_t o = a.xd.o(v);
     W* x = a.x + o;
     const F f = a.f;
-    TFTB_STAMP(a, 0);
     if (a.pre)
         tile_load_pre<F>(a, S, x + cbase, a.pre + o + cbase, n - cbase, C);
     else
         tile_load<W>(S, x + cbase, n - cbase, C, [](uint32_t, W w) { return w; });
     __syncthreads();
-    TFTB_STAMP(a, 1);
     const TwDirect<F> tpi{a.R.Zi, g, CL, f, a.R.ZiM};
     if (g < K) inv_rounds_ct<F, CL, CL, false, TwDirect<F>, false>(f, S, tpi, a.R.ipow2);
     else inv_rounds_ct<F, CL, CL, true>(f, S, tpi, a.R.ipow2, h);
-    TFTB_STAMP(a, 2);
     const uint32_t lim = (uint32_t)min((int64_t)C, n - cbase);
     if (!a.done) {
         tile_store<W>(x + cbase, S, lim, [](W w) { return w; });
@@ -601,11 +595,9 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_cli_chunks(LaunchArgs<F
         if (last) a.done[v - a.vbase] = 0;  // reset for the next execution
     }
     __syncthreads();
-    TFTB_STAMP(a, 3);
     if (!last) return;
     __threadfence();  // acquire: the siblings' rows
     cli_cols_body<F, CL>(a, v, S, false);
-    TFTB_STAMP(a, 7);
 }
 
 template <class F, int CL>
@@ -1167,7 +1159,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_clf_chunks(LaunchArgs<F
     tile_store<W>(x, S, C, [&](W w) { return f.canon(w); });
 }
 
-template <class F, int CL, int GAM, int NR = (1 << GAM)>
+template <class F, int CL, int GAM, int NR = (1 << GAM), bool TIM = false>
 __global__ void __launch_bounds__(256, kern_minb<F>()) k_clg_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     extern __shared__ __align__(16) unsigned char smem_raw[];

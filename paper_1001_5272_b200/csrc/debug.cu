@@ -75,9 +75,9 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
         return 0;
     }
     const int gam = pl.l - CL;
-    void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1>
-                                 : gam == 2 ? (pl.G == 3 ? k_clg_fwd<F30, CL, 2, 3> : k_clg_fwd<F30, CL, 2>)
-                                            : k_clg_fwd<F30, CL, 3>;
+    void (*kg)(LaunchArgs<F30>) = gam == 1 ? k_clg_fwd<F30, CL, 1, 2, true>
+                                 : gam == 2 ? (pl.G == 3 ? k_clg_fwd<F30, CL, 2, 3, true> : k_clg_fwd<F30, CL, 2, 4, true>)
+                                            : k_clg_fwd<F30, CL, 3, 8, true>;
     if (set_smem(kg, smem)) return -1;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(pl.G, (unsigned)count, 1);
