@@ -360,16 +360,89 @@ TFT_DEV uint32_t redc_dot4(const F30& f, const uint32_t* y, const uint32_t* wM, 
     return f.red1((uint32_t)((acc + (uint64_t)q * f.p) >> 32));
 }
 
+// Constants of the small-network column solves (F30): the row scale
+// s = 2^-CL of the split inverse's chunk pass, s/2, s/4, 1/2, 1/4, the
+// point w = omega_2 = Z[1] (omega_0..3 = 1, -1, w, -w), s w^-1 / 4, w^-1 / 4.
+struct SmallNet {
+    Tw<uint32_t> s, s2, s4, h2, h4, w, swi4, wi4;
+};
+
+// The column solve for M <= 4 known outputs as the inverse of the 4-point
+// column network on 1, -1, w, -w, instead of the dense V_M^-1: 3-5 Shoup
+// products instead of M^2 (+ M for the next output).  Rows are scaled by
+// 2^CL except, with LASTS, the last one (the split inverse's convention,
+// vinvS / vinvT).  Outputs canonical; the next output F(omega_M) for M < 4.
+template <int M, bool LASTS>
+TFT_DEV void col_solve_net(const F30& f, const uint32_t* y, const SmallNet& k, uint32_t* xv, uint32_t* nv) {
+    const uint32_t p = f.p, p2 = f.p2;
+    if constexpr (M == 1) {
+        const uint32_t x0 = f.canon(f.mulw(y[0], k.s));
+        xv[0] = x0;
+        if (nv) *nv = x0;
+    } else if constexpr (M == 2) {
+        uint32_t x0, x1;
+        if constexpr (!LASTS) {
+            x0 = f.mulw(y[0] + y[1], k.s2);
+            x1 = f.mulw(y[0] - y[1] + p, k.s2);
+        } else {
+            const uint32_t c0 = f.mulw(y[0], k.s);
+            x0 = f.mulw(c0 + y[1], k.h2);
+            x1 = f.mulw(c0 - y[1] + p, k.h2);
+        }
+        xv[0] = f.canon(x0);
+        xv[1] = f.canon(x1);
+        if (nv) *nv = f.canon(x0 + f.mulw(x1, k.w));  // F(w) = x0 + w x1
+    } else if constexpr (M == 3) {
+        const uint32_t a1 = f.mulw(y[0] - y[1] + p, k.s2);  // x1
+        const uint32_t t = f.mulw(a1, k.w);
+        const uint32_t c2 = LASTS ? y[2] : f.mulw(y[2], k.s);
+        const uint32_t a2 = f.red2(c2 - t + p2);            // x0 - x2
+        const uint32_t m = f.mulw(y[0] + y[1], k.s4), q = f.mulw(a2, k.h2);
+        xv[0] = f.canon(m + q);
+        xv[1] = f.canon(a1);
+        xv[2] = f.canon(m - q + p2);
+        if (nv) *nv = f.canon(a2 - t + p2);                 // F(-w) = (x0 - x2) - w x1
+    } else {
+        static_assert(M == 4, "small column networks have at most 4 points");
+        const uint32_t P = y[0] + y[1], Q = y[0] - y[1] + p;
+        uint32_t x0, x2, m2;
+        if constexpr (!LASTS) {
+            x0 = f.mulw(P + y[2] + y[3], k.s4);
+            x2 = f.mulw(P - (y[2] + y[3]) + p2, k.s4);  // (P, y2 + y3 < 2p: no wrap)
+            m2 = f.mulw(y[2] - y[3] + p, k.swi4);
+        } else {
+            const uint32_t c2 = f.mulw(y[2], k.s);
+            const uint32_t u = f.mulw(P, k.s4), v = f.mulw(c2 + y[3], k.h4);
+            x0 = u + v;
+            x2 = u - v + p2;
+            m2 = f.mulw(c2 - y[3] + p, k.wi4);
+        }
+        const uint32_t m1 = f.mulw(Q, k.s4);
+        xv[0] = f.canon(x0);
+        xv[1] = f.canon(m1 + m2);
+        xv[2] = f.canon(x2);
+        xv[3] = f.canon(m1 - m2 + p2);
+    }
+}
+
 // column solve: y[0..M) are the column's first M outputs; xv <- its M
 // coefficients (V_M^-1, M^2 products, canonical) and, if wanted, nv <- the
-// next output sum_j x_j omega_M^j
-template <class F, int M>
+// next output sum_j x_j omega_M^j.  With sn (F30, M <= 4; M = 4 without a
+// next output) the small-network solve above replaces the dense products.
+template <class F, int M, bool LASTS = false>
 TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typename F::W>* blk,
-                            const typename F::W* blkM, typename F::W* xv, typename F::W* nv) {
+                            const typename F::W* blkM, typename F::W* xv, typename F::W* nv,
+                            const SmallNet* sn = nullptr) {
     using W = typename F::W;
     W y[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) y[j] = f.canon(yin[j]);
+    if constexpr (std::is_same<F, F30>::value && M <= 4) {
+        if (sn && !(M == 4 && nv)) {
+            col_solve_net<M, LASTS>(f, y, *sn, xv, nv);
+            return;
+        }
+    }
     if constexpr (std::is_same<F, F30>::value) {
         // REDC dot products over raw Montgomery entries, <= 4 terms per reduction
 #pragma unroll
@@ -407,15 +480,15 @@ TFT_DEV void col_solve_vals(const F& f, const typename F::W* yin, const Tw<typen
 // to the vector in global memory (row r of column c is x[r C + c]; a warp's
 // stores are 32 consecutive words); with write_next the next output goes to
 // nx(c, value)
-template <class F, int M, class LD, class NX>
+template <class F, int M, bool LASTS = false, class LD, class NX>
 TFT_DEV void col_solve_range(const F& f, const LD& ld, const NX& nx, typename F::W* xg, uint32_t C, uint32_t lo,
                              uint32_t hi, const Tw<typename F::W>* blk, const typename F::W* blkM,
-                             bool write_next) {
+                             bool write_next, const SmallNet* sn = nullptr) {
     using W = typename F::W;
     uint32_t c = lo + threadIdx.x;
     auto one = [&](uint32_t cc, const W* y) {
         W xv[M], nv;
-        col_solve_vals<F, M>(f, y, blk, blkM, xv, write_next ? &nv : nullptr);
+        col_solve_vals<F, M, LASTS>(f, y, blk, blkM, xv, write_next ? &nv : nullptr, sn);
 #pragma unroll
         for (int r = 0; r < M; ++r) xg[(size_t)r * C + cc] = xv[r];
         if (write_next) nx(cc, nv);
@@ -448,20 +521,20 @@ TFT_DEV void col_solve_range(const F& f, const LD& ld, const NX& nx, typename F:
 // through col_solve_range.
 template <class F, int M, bool LASTS, bool NEXT>
 TFT_DEV void colq_solve(const F& f, typename F::W* x, typename F::W* S, uint32_t C, uint32_t clo, uint32_t chi,
-                        const Tw<typename F::W>* blk, const typename F::W* blkM) {
+                        const Tw<typename F::W>* blk, const typename F::W* blkM, const SmallNet* sn = nullptr) {
     using W = typename F::W;
     constexpr int KG = LASTS ? M - 1 : M, QIF = M <= 3 ? 2 : 1;
     auto ld = [&](int j, uint32_t c) { return j < KG ? __ldcg(x + (size_t)j * C + c) : S[c + (c >> 5)]; };
     auto nx = [&](uint32_t c, W w) { S[c + (c >> 5)] = w; };
     if (clo >= chi) return;
     if constexpr (M > 4 || sizeof(W) != 4) {  // (few vectors; registers would spill) scalar loads
-        col_solve_range<F, M>(f, ld, nx, x, C, clo, chi, blk, blkM, NEXT);
+        col_solve_range<F, M, LASTS>(f, ld, nx, x, C, clo, chi, blk, blkM, NEXT, sn);
         return;
     }
     const uint32_t mis = (uint32_t)(((uintptr_t)(x + clo) & 15) / sizeof(W));
     const uint32_t head = min(chi - clo, (4 - mis) & 3);
     const uint32_t c_a = clo + head, nq = (chi - c_a) / 4, c_b = c_a + 4 * nq;
-    if (head) col_solve_range<F, M>(f, ld, nx, x, C, clo, c_a, blk, blkM, NEXT);
+    if (head) col_solve_range<F, M, LASTS>(f, ld, nx, x, C, clo, c_a, blk, blkM, NEXT, sn);
     for (uint32_t q0 = threadIdx.x; q0 < nq; q0 += QIF * blockDim.x) {
         uint4 r[QIF][KG];
 #pragma unroll
@@ -483,7 +556,7 @@ TFT_DEV void colq_solve(const F& f, typename F::W* x, typename F::W* S, uint32_t
                 for (int j = 0; j < KG; ++j) y[j] = k == 0 ? r[u][j].x : k == 1 ? r[u][j].y : k == 2 ? r[u][j].z : r[u][j].w;
                 const uint32_t c = c0 + k;
                 if (LASTS) y[M - 1] = S[c + (c >> 5)];
-                col_solve_vals<F, M>(f, y, blk, blkM, xv, NEXT ? &nv : nullptr);
+                col_solve_vals<F, M, LASTS>(f, y, blk, blkM, xv, NEXT ? &nv : nullptr, sn);
                 if (NEXT) S[c + (c >> 5)] = nv;
 #pragma unroll
                 for (int j = 0; j < M; ++j) out[j][k] = xv[j];
@@ -493,7 +566,7 @@ TFT_DEV void colq_solve(const F& f, typename F::W* x, typename F::W* S, uint32_t
                 *reinterpret_cast<uint4*>(x + (size_t)j * C + c0) = make_uint4(out[j][0], out[j][1], out[j][2], out[j][3]);
         }
     }
-    if (c_b < chi) col_solve_range<F, M>(f, ld, nx, x, C, c_b, chi, blk, blkM, NEXT);
+    if (c_b < chi) col_solve_range<F, M, LASTS>(f, ld, nx, x, C, c_b, chi, blk, blkM, NEXT, sn);
 }
 
 // Split inverse for 2^CL < n <= 8 2^CL (no cluster): two launches.
@@ -521,11 +594,20 @@ TFT_DEV void cli_cols_body(const LaunchArgs<F>& a, int64_t v, typename F::W* S, 
     if (prefetch && threadIdx.x == 0) l2_prefetch(x, n);
     const Tw<W>* b1 = a.R.vinvS + 72 * (K - 1);
     const W* b1M = a.R.vinvM + 8 * 72 + 72 * (K - 1);
+    // small-network solves (F30): the scale and point constants, per thread
+    SmallNet snv{};
+    const SmallNet* sn = nullptr;
+    if constexpr (std::is_same<F, F30>::value) {
+        const Tw<W>* ip = a.R.ipow2;
+        snv = SmallNet{ip[CL], ip[CL + 1], ip[CL + 2], ip[1], ip[2], a.R.Zf[1],
+                       f.tw(f.twmul(a.R.Zi[1], ip[CL + 2])), f.tw(f.twmul(a.R.Zi[1], ip[2]))};
+        if (!a.dense_cols) sn = &snv;
+    }
     switch (K) {  // columns >= h: K rows
 #define TFTB_C1(k)                                                                          \
     case k:                                                                                 \
-        if (h) colq_solve<F, k, false, true>(f, x, S, C, h, C, b1, b1M);                    \
-        else colq_solve<F, k, false, false>(f, x, S, C, 0, C, b1, b1M);                     \
+        if (h) colq_solve<F, k, false, true>(f, x, S, C, h, C, b1, b1M, sn);                \
+        else colq_solve<F, k, false, false>(f, x, S, C, 0, C, b1, b1M, sn);                 \
         break;
         TFTB_C1(1) TFTB_C1(2) TFTB_C1(3) TFTB_C1(4) TFTB_C1(5) TFTB_C1(6) TFTB_C1(7)
         default: colq_solve<F, 8, false, false>(f, x, S, C, 0, C, b1, b1M); break;  // K = 8: h = 0
@@ -542,7 +624,7 @@ TFT_DEV void cli_cols_body(const LaunchArgs<F>& a, int64_t v, typename F::W* S, 
     const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
     switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
 #define TFTB_C2(m)                                                                          \
-    case m: colq_solve<F, m, true, false>(f, x, S, C, 0, h, b2, b2M); break;
+    case m: colq_solve<F, m, true, false>(f, x, S, C, 0, h, b2, b2M, sn); break;
         TFTB_C2(2) TFTB_C2(3) TFTB_C2(4) TFTB_C2(5) TFTB_C2(6) TFTB_C2(7) TFTB_C2(8)
 #undef TFTB_C2
     }

@@ -133,6 +133,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     a.in = in ? in : x;
     a.ind = in ? ind : xd;
     a.pre = pre;
+    static const int dense_cols = getenv("TFTB_DENSE_COLS") != nullptr;  // A/B knob
+    a.dense_cols = dense_cols;
     a.l0 = pl.l0;
     a.l1 = pl.l1;
     a.wlog = pl.wlog;

@@ -50,6 +50,7 @@ struct LaunchArgs {
     int64_t vbase;        // first vector of this launch
     unsigned long long* timing;  // debug: per-CTA phase timestamps (null in production)
     unsigned* done;              // per-vector chunk tickets (fused split inverse), v - vbase
+    int dense_cols;              // A/B: dense V^-1 column solves (TFTB_DENSE_COLS)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
