@@ -619,7 +619,7 @@ TFT_DEV void cli_cols_body(const LaunchArgs<F>& a, int64_t v, typename F::W* S, 
     tile_load<W>(S, x + (size_t)K * C, h, h, [](uint32_t, W w) { return w; });
     __syncthreads();
     const TwDirect<F> tpi{a.R.Zi, K, CL, f, a.R.ZiM};
-    itft_phases23(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
+    itft_phases23<0>(f, SmemTile<W>{S, CL, 0}, h, TwDirect<F>{a.R.Zf, K, CL, f}, tpi, a.R);
     const Tw<W>* b2 = a.R.vinvT + 72 * K;
     const W* b2M = a.R.vinvM + 16 * 72 + 72 * K;
     switch (K + 1) {  // columns < h: K + 1 rows, the last from the tile
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_last_inv(LaunchArgs<F> 
     __syncthreads();
     const TwBig<F> tpf{a.R.Zf, a.R.Zfh, K, CL, a.R.zb, f}, tpi{a.R.Zi, a.R.Zih, K, CL, a.R.zb, f};
     SmemTile<W> tl{S, CL, 0};
-    itft_phases23(f, tl, h, tpf, tpi, a.R);
+    itft_phases23<0>(f, tl, h, tpf, tpi, a.R);
     tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });
 }
 
@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     const TwPrefix<F> tpf{a.R.Zf}, tpi{a.R.Zi};
     inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, WLOG>(f, S, tpi, a.R.ipow2, rows);
     SmemTile<W> tl{S, L0, WLOG};
-    itft_phases23(f, tl, rows, tpf, tpi, a.R);
+    itft_phases23<WLOG>(f, tl, rows, tpf, tpi, a.R);
     for (uint32_t g = threadIdx.x; g < (rows << WLOG); g += blockDim.x) {
         const uint32_t r = g >> WLOG, c = c0 + (g & (NC - 1));
         const int64_t pos = (int64_t)r * C + c;

@@ -170,13 +170,22 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
 //   3. bottom-up: recombine the halves with one inverse butterfly.
 // Same values as the reference's Algorithm 2 since the
 // inverse map is unique; the odd-tail Horner passes are not needed.
-template <class F, class TPF, class TPI>
+//
+// WL >= 0: the tile's column count 2^WL known at compile time (every caller:
+// single-column tiles and chunks WL = 0, two-pass column tiles their WLOG),
+// so the per-element index arithmetic folds to constants.
+template <int WL = -1, class F, class TPF, class TPI>
 TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
                       const TPI& tpi, const RingDev<typename F::W>& R, Lanes ln = cta_lanes(),
                       bool uniform = false) {
     using W = typename F::W;
     const int t = tl.t;
-    const uint32_t ncols = 1u << tl.wlog;
+    const int wl = WL >= 0 ? WL : wl;
+    const uint32_t ncols = 1u << wl;
+    auto at = [&](uint32_t pos, uint32_t col) -> W& {
+        const uint32_t idx = (pos << wl) | col;
+        return tl.S[idx + (idx >> 5)];
+    };
     // uniform: every tile of the CTA walks all levels (the barriers must
     // match); tiles with nothing to do at a level just skip its work
     const bool act = h != 0 && h < (1u << t);
@@ -215,31 +224,31 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
             if (hd >= H) {
-                const uint32_t i0 = hd - H, cnt = (H - i0) << tl.wlog;
+                const uint32_t i0 = hd - H, cnt = (H - i0) << wl;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = i0 + (g >> tl.wlog);
-                    W tv = tl.at(tl.ix(B + H + i, col));
+                    uint32_t col = g & (ncols - 1), i = i0 + (g >> wl);
+                    W tv = at(B + H + i, col);
                     if constexpr (F::kLazy) {  // values stay in [0, 4p)
                         const W m = f.mulw(tv, w);
-                        const W x = f.red2(tl.at(tl.ix(B + i, col))) - m + f.p2;
-                        tl.at(tl.ix(B + i, col)) = x;
-                        tl.at(tl.ix(B + H + i, col)) = f.red2(x) - m + f.p2;
+                        const W x = f.red2(at(B + i, col)) - m + f.p2;
+                        at(B + i, col) = x;
+                        at(B + H + i, col) = f.red2(x) - m + f.p2;
                     } else {
-                        W lo = f.canon(tl.at(tl.ix(B + i, col)));
+                        W lo = f.canon(at(B + i, col));
                         W m = f.cmulw(tv, w);
                         W x = f.csub(lo, m);
-                        tl.at(tl.ix(B + i, col)) = x;
-                        tl.at(tl.ix(B + H + i, col)) = f.csub(x, m);
+                        at(B + i, col) = x;
+                        at(B + H + i, col) = f.csub(x, m);
                     }
                 }
             } else {
-                const uint32_t cnt = (H - hd) << tl.wlog;
+                const uint32_t cnt = (H - hd) << wl;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = hd + (g >> tl.wlog);
-                    W a = tl.at(tl.ix(B + i, col));
-                    W b = tl.at(tl.ix(B + H + i, col));
-                    if constexpr (F::kLazy) tl.at(tl.ix(B + i, col)) = f.red2(a) + f.mulw(b, w);
-                    else tl.at(tl.ix(B + i, col)) = f.cadd(a, f.cmulw(b, w));
+                    uint32_t col = g & (ncols - 1), i = hd + (g >> wl);
+                    W a = at(B + i, col);
+                    W b = at(B + H + i, col);
+                    if constexpr (F::kLazy) at(B + i, col) = f.red2(a) + f.mulw(b, w);
+                    else at(B + i, col) = f.cadd(a, f.cmulw(b, w));
                 }
             }
         }
@@ -252,30 +261,30 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
             if (hd >= H) {
-                const uint32_t cnt = (hd - H) << tl.wlog;
+                const uint32_t cnt = (hd - H) << wl;
                 const Tw<W> wh = cnt ? f.tw(f.twmul(w, R.inv2)) : w;  // w / 2: one product per element
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
+                    uint32_t col = g & (ncols - 1), i = g >> wl;
                     if constexpr (F::kLazy) {
-                        const W lo = f.red2(tl.at(tl.ix(B + i, col)));
-                        const W hi = f.red2(tl.at(tl.ix(B + H + i, col)));
-                        tl.at(tl.ix(B + i, col)) = f.mulw(lo + hi, R.inv2);
-                        tl.at(tl.ix(B + H + i, col)) = f.mulw(lo - hi + f.p2, wh);
+                        const W lo = f.red2(at(B + i, col));
+                        const W hi = f.red2(at(B + H + i, col));
+                        at(B + i, col) = f.mulw(lo + hi, R.inv2);
+                        at(B + H + i, col) = f.mulw(lo - hi + f.p2, wh);
                     } else {
-                        W lo = f.canon(tl.at(tl.ix(B + i, col)));
-                        W hi = tl.at(tl.ix(B + H + i, col));
-                        tl.at(tl.ix(B + i, col)) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                        tl.at(tl.ix(B + H + i, col)) = f.cmulw(f.csub(lo, hi), wh);
+                        W lo = f.canon(at(B + i, col));
+                        W hi = at(B + H + i, col);
+                        at(B + i, col) = f.cmulw(f.cadd(lo, hi), R.inv2);
+                        at(B + H + i, col) = f.cmulw(f.csub(lo, hi), wh);
                     }
                 }
             } else {
-                const uint32_t cnt = hd << tl.wlog;
+                const uint32_t cnt = hd << wl;
                 for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = g >> tl.wlog;
-                    W a = tl.at(tl.ix(B + i, col));
-                    W b = tl.at(tl.ix(B + H + i, col));
-                    if constexpr (F::kLazy) tl.at(tl.ix(B + i, col)) = f.red2(a) - f.mulw(b, w) + f.p2;
-                    else tl.at(tl.ix(B + i, col)) = f.csub(a, f.cmulw(b, w));
+                    uint32_t col = g & (ncols - 1), i = g >> wl;
+                    W a = at(B + i, col);
+                    W b = at(B + H + i, col);
+                    if constexpr (F::kLazy) at(B + i, col) = f.red2(a) - f.mulw(b, w) + f.p2;
+                    else at(B + i, col) = f.csub(a, f.cmulw(b, w));
                 }
             }
         }
