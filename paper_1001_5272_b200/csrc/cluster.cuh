@@ -851,6 +851,43 @@ TFT_DEV void col_load(W* S, const W* src, uint32_t C, int64_t avail, const XF& x
     }
 }
 
+// x_t[r C + c] = canon(S[(r << WLOG) | c]) for rows [r0, r1) and tile columns
+// [clo, chi) (x_t = the tile's first column in the vector).  Whole-width
+// stores of 16-byte-aligned rows go out as 16-byte vectors (rows share the
+// alignment of x_t: C is a multiple of the vector width); edges scalar.
+// Plain stores: the other pass reads these words next, often from L2.
+template <class F, int WLOG>
+TFT_DEV void col_store(const F& f, typename F::W* xt, const typename F::W* S, uint32_t C, uint32_t r0, uint32_t r1,
+                       uint32_t clo, uint32_t chi) {
+    using W = typename F::W;
+    using V = Vec16<W>;
+    constexpr int NV = V::N;
+    constexpr uint32_t NC = 1u << WLOG;
+    if (r1 <= r0 || chi <= clo) return;
+    if constexpr (NC >= (uint32_t)NV) {
+        if (clo == 0 && chi == NC && ((uintptr_t)xt & 15) == 0) {
+            constexpr uint32_t QR = NC / NV;  // vectors per row
+            const uint32_t nq = (r1 - r0) * QR;
+            for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+                const uint32_t r = r0 + q / QR, c = (q % QR) * NV;
+                const uint32_t idx = (r << WLOG) | c;
+                const W* s = S + idx + (idx >> 5);  // (NV words inside one padded 32-word row)
+                W e[NV];
+#pragma unroll
+                for (int k = 0; k < NV; ++k) e[k] = f.canon(s[k]);
+                *reinterpret_cast<typename V::T*>(xt + (size_t)r * C + c) = V::make(e);
+            }
+            return;
+        }
+    }
+    const uint32_t w = chi - clo, cnt = (r1 - r0) * w;
+    for (uint32_t g = threadIdx.x; g < cnt; g += blockDim.x) {
+        const uint32_t r = r0 + g / w, c = clo + g % w;
+        const uint32_t idx = (r << WLOG) | c;
+        xt[(size_t)r * C + c] = f.canon(S[idx + (idx >> 5)]);
+    }
+}
+
 template <class F, int L0>
 __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
@@ -871,12 +908,16 @@ __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
     // rows <= K are the only outputs (row K: real for c < h, the stash for c >= h)
     fwd_rounds_ct<F, L0, L0, WLOG, true>(f, S, TwPrefix<F>{a.R.Zf}, K + (h ? 1u : 0u));
     const uint32_t NC = 1u << WLOG;
-    W* st = a.stash + (v - a.vbase) * (int64_t)C;
-    for (uint32_t g = threadIdx.x; g < ((K + 1) << WLOG) && g < (1u << (L0 + WLOG)); g += blockDim.x) {
-        const uint32_t r = g >> WLOG, c = c0 + (g & (NC - 1));
-        const int64_t pos = (int64_t)r * C + c;
-        if (pos < n) x[pos] = f.canon(S[g + (g >> 5)]);
-        else if (h && r == K) st[c] = f.canon(S[g + (g >> 5)]);
+    // complete rows r < K, then row K: real words for c < h, the stash for c >= h
+    col_store<F, WLOG>(f, x + c0, S, C, 0, min(K, 1u << L0), 0, NC);
+    if (h && K < (1u << L0)) {
+        W* st = a.stash + (v - a.vbase) * (int64_t)C;
+        for (uint32_t col = threadIdx.x; col < NC; col += blockDim.x) {
+            const uint32_t c = c0 + col, g = (K << WLOG) | col;
+            const W w = f.canon(S[g + (g >> 5)]);
+            if (c < h) x[(size_t)K * C + c] = w;
+            else st[c] = w;
+        }
     }
 }
 
@@ -914,11 +955,8 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, WLOG>(f, S, tpi, a.R.ipow2, rows);
     SmemTile<W> tl{S, L0, WLOG};
     itft_phases23<WLOG>(f, tl, rows, tpf, tpi, a.R);
-    for (uint32_t g = threadIdx.x; g < (rows << WLOG); g += blockDim.x) {
-        const uint32_t r = g >> WLOG, c = c0 + (g & (NC - 1));
-        const int64_t pos = (int64_t)r * C + c;
-        if (c >= lo && c < hi && pos < n) x[pos] = f.canon(S[g + (g >> 5)]);
-    }
+    // (every position of rows < rows in [lo, hi) is < n: row K only for c < h)
+    col_store<F, WLOG>(f, x + c0, S, C, 0, rows, max(lo, c0) - c0, min(hi, c0 + NC) - c0);
     if (which == 0 && h) {
         W* red = S + padded_words(1u << (L0 + WLOG));
         W* nv = red + blockDim.x;
