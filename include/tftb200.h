@@ -131,6 +131,13 @@ int64_t tftb_launch_count(int reset);
  * the n-word buffer alone. */
 int64_t tftb_aux_bytes(int reset);
 
+/* High-water mark of the device bytes this thread's host-pointer calls
+ * (tftb_tft_u64 / tftb_itft_u64 / tftb_multiply_u64 / tftb_tft_batch_u64)
+ * allocated for the caller's words since the last reset: the ring words
+ * (4 B per word for p < 2^32) plus a bounded conversion staging (32 MB per
+ * call, three sub-batches for the host batch), not 12 B per word. */
+int64_t tftb_stage_bytes(int reset);
+
 /* ------------------------------------------------------------ op tallies
  * (mults, adds) the reference walk reports for the same call: the second
  * tuple element of _kernels.tft / _kernels.itft (_kernels.pyx:415-430) and

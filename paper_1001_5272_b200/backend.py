@@ -64,6 +64,7 @@ SIGNATURES = {
     "tftb_version": (ctypes.c_char_p, []),
     "tftb_launch_count": (ctypes.c_int64, [ctypes.c_int]),
     "tftb_aux_bytes": (ctypes.c_int64, [ctypes.c_int]),
+    "tftb_stage_bytes": (ctypes.c_int64, [ctypes.c_int]),
     "tftb_tally_transform": (ctypes.c_int, [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _i64p, _i64p]),
     "tftb_tally_multiply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, _i64p,
                                            _i64p]),
@@ -170,6 +171,12 @@ def ring_handle(cfg):
 
 def launch_count(reset=False):
     return int(load().tftb_launch_count(1 if reset else 0))
+
+
+def stage_bytes(reset=False):
+    """Device bytes this thread's host-pointer calls allocated for the
+    caller's words (high-water mark since the last reset)."""
+    return int(load().tftb_stage_bytes(1 if reset else 0))
 
 
 def aux_bytes(reset=False):

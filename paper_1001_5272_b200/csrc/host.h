@@ -28,6 +28,9 @@ extern thread_local int64_t g_launches;
 // partials, the product's second operand): current and high-water mark of
 // this thread's calls -- the footprint audit (tftb_aux_bytes)
 extern thread_local int64_t g_aux_cur, g_aux_peak;
+// device bytes the host-pointer entry points allocate for the caller's words
+// (ring words + conversion staging): current and high-water mark
+extern thread_local int64_t g_stage_cur, g_stage_peak;
 
 inline int fail(const std::string& msg) {
     g_err = msg;
@@ -204,12 +207,16 @@ struct Scratch {
         if (aux) {
             g_aux_cur += (int64_t)b;
             g_aux_peak = std::max(g_aux_peak, g_aux_cur);
+        } else {
+            g_stage_cur += (int64_t)b;
+            g_stage_peak = std::max(g_stage_peak, g_stage_cur);
         }
         return 0;
     }
     ~Scratch() {
         if (p) cudaFreeAsync(p, s);
         if (p && aux) g_aux_cur -= (int64_t)bytes;
+        if (p && !aux) g_stage_cur -= (int64_t)bytes;
     }
 };
 

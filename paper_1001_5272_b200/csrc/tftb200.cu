@@ -23,6 +23,7 @@ namespace tftb {
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 thread_local int64_t g_aux_cur = 0, g_aux_peak = 0;
+thread_local int64_t g_stage_cur = 0, g_stage_peak = 0;
 
 template <typename W>
 struct TableBuilder {
@@ -298,6 +299,45 @@ struct CtxLease {
 };
 
 // model op counts of the device algorithm
+// Host uint64 words <-> device words of a u32 ring through a bounded u64
+// staging buffer (kStageWords): device memory is the ring words (4 B/word)
+// plus the staging, not 12 B/word.  The pieces are stream-ordered on st, so
+// the staging is reused safely; PCIe dominates, the conversion kernels are
+// small.  u64 rings copy straight into their words.
+constexpr int64_t kStageWords = 1 << 22;  // 32 MB
+
+template <typename W>
+int upload_words(W* d, const uint64_t* h, int64_t n, uint64_t* stage, cudaStream_t st) {
+    if constexpr (sizeof(W) == 8) {
+        CK(cudaMemcpyAsync(d, h, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    } else {
+        for (int64_t i = 0; i < n; i += kStageWords) {
+            const int64_t m = std::min(kStageWords, n - i);
+            CK(cudaMemcpyAsync(stage, h + i, (size_t)m * 8, cudaMemcpyHostToDevice, st));
+            const int nb = (int)std::min<int64_t>((m + 255) / 256, 148 * 16);
+            k_u64_to_w<W><<<nb, 256, 0, st>>>(stage, d + i, m);
+            g_launches++;
+        }
+    }
+    return 0;
+}
+
+template <typename W>
+int download_words(uint64_t* h, const W* d, int64_t n, uint64_t* stage, cudaStream_t st) {
+    if constexpr (sizeof(W) == 8) {
+        CK(cudaMemcpyAsync(h, d, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+        for (int64_t i = 0; i < n; i += kStageWords) {
+            const int64_t m = std::min(kStageWords, n - i);
+            const int nb = (int)std::min<int64_t>((m + 255) / 256, 148 * 16);
+            k_w_to_u64<W><<<nb, 256, 0, st>>>(d + i, stage, m);
+            g_launches++;
+            CK(cudaMemcpyAsync(h + i, stage, (size_t)m * 8, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    return 0;
+}
+
 int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, bool inverse, int64_t* mults,
                     int64_t* adds) {
     if (n <= 0) return fail("cannot transform an empty buffer");
@@ -308,31 +348,32 @@ int host_tft_common(uint64_t* x, int64_t n, uint64_t p, uint64_t top, int K, boo
     if (lease.acquire()) return -1;
     cudaStream_t st = lease.stream();
     const size_t wb = rh->wbytes;
+    // device: the n ring words, plus (u32 rings) a bounded u64 staging
+    const int64_t sw = wb == 4 ? std::min(n, kStageWords) : 0;
+    const size_t wbytes = ((size_t)n * wb + 255) & ~(size_t)255;
     Scratch buf;
-    if (buf.get((size_t)n * 8 + (wb == 4 ? (size_t)n * 4 : 0), st)) return -1;
-    uint64_t* d64 = (uint64_t*)buf.p;
+    if (buf.get(wbytes + (size_t)sw * 8, st)) return -1;
+    void* dw = buf.p;
+    uint64_t* stage = (uint64_t*)((char*)buf.p + wbytes);
     uint64_t* hx = x;
     if ((size_t)n * 8 <= kPinMax && !host_pinned(x)) {
         if (lease.c->pin_reserve((size_t)n * 8)) return -1;
         hx = (uint64_t*)lease.c->pin;
         memcpy(hx, x, (size_t)n * 8);
     }
-    CK(cudaMemcpyAsync(d64, hx, (size_t)n * 8, cudaMemcpyHostToDevice, st));
     int rc = 0;
     if (wb == 4) {
-        uint32_t* dw = (uint32_t*)(d64 + n);
-        int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-        k_u64_to_w<uint32_t><<<nb, 256, 0, st>>>(d64, dw, n);
+        if (upload_words((uint32_t*)dw, hx, n, stage, st)) return -1;
         rc = rh->kind == 0 ? dispatch_tft<F30>(rh, dw, 1, n, n, nullptr, nullptr, inverse, st)
                            : dispatch_tft<F32>(rh, dw, 1, n, n, nullptr, nullptr, inverse, st);
         if (rc) return rc;
-        k_w_to_u64<uint32_t><<<nb, 256, 0, st>>>(dw, d64, n);
-        g_launches += 2;
+        if (download_words(hx, (const uint32_t*)dw, n, stage, st)) return -1;
     } else {
-        rc = dispatch_tft<F62>(rh, d64, 1, n, n, nullptr, nullptr, inverse, st);
+        if (upload_words((uint64_t*)dw, hx, n, stage, st)) return -1;
+        rc = dispatch_tft<F62>(rh, dw, 1, n, n, nullptr, nullptr, inverse, st);
         if (rc) return rc;
+        if (download_words(hx, (const uint64_t*)dw, n, stage, st)) return -1;
     }
-    CK(cudaMemcpyAsync(hx, d64, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (hx != x) memcpy(x, hx, (size_t)n * 8);
     tally_transform(n, p, K, inverse, mults, adds);
@@ -369,15 +410,16 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
     if (lease.acquire()) return -1;
     cudaStream_t st = lease.stream();
     const size_t wb = rh->wbytes;
-    // device: a, b, x as u64 staging + (u32 field) word copies + the Y scratch
+    // device: a, b, x and the Y scratch as ring words, plus (u32 rings) a
+    // bounded u64 staging for the conversions
+    const size_t words = (size_t)(la + lb + 2 * r);
+    const size_t wbytes = (words * wb + 255) & ~(size_t)255;
+    const int64_t sw = wb == 4 ? std::min<int64_t>(std::max(la + lb, r), kStageWords) : 0;
     Scratch buf;
-    size_t words64 = (size_t)(la + lb + r);
-    if (buf.get(words64 * 8 + (size_t)(la + lb + 2 * r) * wb, st)) return -1;
-    uint64_t* da64 = (uint64_t*)buf.p;
-    uint64_t* db64 = da64 + la;
-    uint64_t* dx64 = db64 + lb;
-    unsigned char* wbase = (unsigned char*)(dx64 + r);
+    if (buf.get(wbytes + (size_t)sw * 8, st)) return -1;
+    uint64_t* stage = (uint64_t*)((char*)buf.p + wbytes);
     // pinned staging for pageable callers: [a | b | x]
+    const size_t words64 = (size_t)(la + lb + r);
     const uint64_t* ha = a;
     const uint64_t* hb = b;
     uint64_t* hx = x;
@@ -390,26 +432,27 @@ int tftb_multiply_u64(const uint64_t* a, int64_t la, const uint64_t* b, int64_t 
         hb = hp + la;
         hx = hp + la + lb;
     }
-    CK(cudaMemcpyAsync(da64, ha, (size_t)la * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db64, hb, (size_t)lb * 8, cudaMemcpyHostToDevice, st));
     int rc;
     if (wb == 4) {
-        uint32_t* da = (uint32_t*)wbase;
+        uint32_t* da = (uint32_t*)buf.p;
         uint32_t* db = da + la;
         uint32_t* dx = db + lb;
         uint32_t* dy = dx + r;
-        k_u64_to_w<uint32_t><<<592, 256, 0, st>>>(da64, da, la + lb);  // a and b are adjacent
+        if (upload_words(da, ha, la, stage, st) || upload_words(db, hb, lb, stage, st)) return -1;
         rc = rh->kind == 0 ? dispatch_mul<F30>(rh, da, la, la, db, lb, lb, dx, r, 1, dy, st)
                            : dispatch_mul<F32>(rh, da, la, la, db, lb, lb, dx, r, 1, dy, st);
         if (rc) return rc;
-        k_w_to_u64<uint32_t><<<592, 256, 0, st>>>(dx, dx64, r);
-        g_launches += 2;
+        if (download_words(hx, dx, r, stage, st)) return -1;
     } else {
-        uint64_t* dy = (uint64_t*)wbase;
-        rc = dispatch_mul<F62>(rh, da64, la, la, db64, lb, lb, dx64, r, 1, dy, st);
+        uint64_t* da = (uint64_t*)buf.p;
+        uint64_t* db = da + la;
+        uint64_t* dx = db + lb;
+        uint64_t* dy = dx + r;
+        if (upload_words(da, ha, la, stage, st) || upload_words(db, hb, lb, stage, st)) return -1;
+        rc = dispatch_mul<F62>(rh, da, la, la, db, lb, lb, dx, r, 1, dy, st);
         if (rc) return rc;
+        if (download_words(hx, dx, r, stage, st)) return -1;
     }
-    CK(cudaMemcpyAsync(hx, dx64, (size_t)r * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (hx != x) memcpy(x, hx, (size_t)r * 8);
     tally_multiply(la, lb, p, K, mults, adds);
@@ -735,6 +778,12 @@ const char* tftb_version(void) { return "tftb200 0.1.0 (sm_100a)"; }
 int64_t tftb_launch_count(int reset) {
     int64_t v = g_launches;
     if (reset) g_launches = 0;
+    return v;
+}
+
+int64_t tftb_stage_bytes(int reset) {
+    const int64_t v = g_stage_peak;
+    if (reset) g_stage_peak = g_stage_cur;
     return v;
 }
 

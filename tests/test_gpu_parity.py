@@ -496,3 +496,26 @@ def test_host_batch_with_gaps_and_unsorted_offsets():
     rc = lib.tftb_tft_batch_u64(buf.ctypes.data, bad.ctypes.data_as(p64), lens[:2].copy().ctypes.data_as(p64),
                                 2, cfg.p, cfg.omegaK, cfg.K, 0)
     assert rc != 0 and b"overlap" in lib.tftb_last_error()
+
+
+@pytest.mark.gpu
+def test_host_api_device_memory_is_the_ring_words_plus_bounded_staging():
+    """The host-pointer calls convert uint64 words through a bounded staging
+    buffer: device memory ~ 4 B per word for u32 rings (+ 32 MB), 8 B for u64."""
+    cfg = T.default_config()
+    for n in (1000, 70001, 3 << 21):
+        x = gen(n, cfg.p, n)
+        backend.stage_bytes(reset=True)
+        y = x.copy()
+        T.tft(y, cfg)
+        T.itft(y, cfg)
+        assert np.array_equal(y, x)
+        used = backend.stage_bytes()
+        assert used <= 4 * n + 8 * min(n, 1 << 22) + 512, (n, used)
+    a, b = gen(1, cfg.p, 1 << 20), gen(2, cfg.p, 1 << 20)
+    out = np.zeros(a.size + b.size - 1, dtype=np.uint64)
+    backend.stage_bytes(reset=True)
+    T.multiply(a, b, out, cfg)
+    r = out.size
+    assert backend.stage_bytes() <= 4 * (a.size + b.size + 2 * r) + 8 * min(r, 1 << 22) + 512
+    assert int(out[0]) == int(a[0]) * int(b[0]) % cfg.p
