@@ -230,6 +230,10 @@ TFT_DEV void fwd_round_units(const F& f, typename F::W* S, const TP& tp, uint32_
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];
         reg_fwd<F, KK, KK - 1>(f, v, base, SLO, tp);
+        if constexpr (is_wide<F>::value) {
+#pragma unroll
+            for (int i = 0; i < (1 << KK); ++i) v[i] = f.narrow(v[i]);
+        }
 #pragma unroll
         for (int i = 0; i < (1 << KK); ++i) pb[unit_off<SLO, WLOG, KK>(i)] = v[i];
     }
@@ -269,6 +273,10 @@ TFT_DEV void inv_round_units(const F& f, typename F::W* S, const TP& tp, const T
         } else {
             reg_inv<F, KK, 0, false>(f, v, base, SLO, tp, h, SCALE ? TL - 1 : -1, ipow2);
         }
+        if constexpr (is_wide<F>::value) {
+#pragma unroll
+            for (int i = 0; i < (1 << KK); ++i) v[i] = f.narrow(v[i]);
+        }
         if constexpr (MASK) {
             // only rows < h change; the rest is not written back
 #pragma unroll
@@ -295,6 +303,14 @@ __host__ __device__ constexpr bool bottom_words() {
 template <class F>
 TFT_DEV auto bottom_field(const F& f) {
     if constexpr (std::is_same<F, F30>::value) return F30M(f);
+    else if constexpr (std::is_same<F, F32>::value) return F32W(f);
+    else return f;
+}
+// the field a register round computes in: F32 rounds run on wide words
+// (field.cuh F32W) and narrow them when the unit is written back
+template <class F>
+TFT_DEV auto round_field(const F& f) {
+    if constexpr (std::is_same<F, F32>::value) return F32W(f);
     else return f;
 }
 
@@ -304,7 +320,8 @@ TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t n
         const auto fb = bottom_field(f);
         fwd_round_units<decltype(fb), TL, KK, SLO, WLOG, PRUNE>(fb, S, tp.mont(), need, ln);
     } else {
-        fwd_round_units<F, TL, KK, SLO, WLOG, PRUNE>(f, S, tp, need, ln);
+        const auto fr = round_field(f);
+        fwd_round_units<decltype(fr), TL, KK, SLO, WLOG, PRUNE>(fr, S, tp, need, ln);
     }
 }
 
@@ -315,7 +332,8 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
         const auto fb = bottom_field(f);
         inv_round_units<decltype(fb), TL, KK, SLO, WLOG, MASK, SCALE>(fb, S, tp.mont(), ipow2, h, ln);
     } else {
-        inv_round_units<F, TL, KK, SLO, WLOG, MASK, SCALE>(f, S, tp, ipow2, h, ln);
+        const auto fr = round_field(f);
+        inv_round_units<decltype(fr), TL, KK, SLO, WLOG, MASK, SCALE>(fr, S, tp, ipow2, h, ln);
     }
 }
 

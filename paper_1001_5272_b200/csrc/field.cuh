@@ -23,6 +23,7 @@
 // Reference: the scalar `(u128)a*b % p` of `_kernels.pyx:17-18`.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #define TFT_DEV __device__ __forceinline__
 
@@ -179,6 +180,56 @@ struct F32 {
         y = mulw(csub(a, b), t);
     }
 };
+
+// F32 inside a register round: words are "wide" -- any 32-bit value
+// congruent to the residue (2^32 < 2p, so a wide word is the canonical one or
+// canonical + p).  The Montgomery product takes any 32-bit multiplicand and
+// returns a canonical word, so a butterfly's sum and difference each need only
+// the carry (borrow) of one 32-bit add and a predicated +-p: ptxas turns the
+// add.cc / addc / setp / @p sequence below into IADD3 (carry predicate) +
+// predicated IMAD.IADD.  Per butterfly 5 ALU-pipe + 7 FMA-pipe slots against
+// the canonical form's 9 + 6 (cuobjdump, tools/cu/f32wide.cu).  Words are made
+// canonical again (narrow) when a round writes its unit back, so tiles in
+// shared memory and everything outside the rounds stay canonical.
+struct F32W : F32 {
+    static constexpr bool kWide = true;
+    TFT_DEV explicit F32W(const F32& f) : F32(f) {}
+    // a wide, b canonical -> wide
+    TFT_DEV W addw(W a, W b) const {
+        W d;
+        asm("{.reg .u32 m; .reg .pred q;\n\t"
+            "add.cc.u32 %0, %1, %2;\n\taddc.u32 m, 0, 0;\n\tsetp.ne.u32 q, m, 0;\n\t"
+            "@q sub.u32 %0, %0, %3;}"
+            : "=&r"(d) : "r"(a), "r"(b), "r"(p));
+        return d;
+    }
+    TFT_DEV W subw(W a, W b) const {
+        W d;
+        asm("{.reg .u32 m; .reg .pred q;\n\t"
+            "sub.cc.u32 %0, %1, %2;\n\taddc.u32 m, 0, 0;\n\tsetp.eq.u32 q, m, 0;\n\t"
+            "@q add.u32 %0, %0, %3;}"
+            : "=&r"(d) : "r"(a), "r"(b), "r"(p));
+        return d;
+    }
+    TFT_DEV W narrow(W x) const { return min(x, x - p); }
+    TFT_DEV void fwd(W& x, W& y, Tw<W> t) const {
+        const W b = mulw(y, t);
+        const W a = x;
+        x = addw(a, b);
+        y = subw(a, b);
+    }
+    TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
+        const W a = x, b = narrow(y);
+        x = addw(a, b);
+        y = mulw(subw(a, b), t);
+    }
+};
+
+// fields whose register rounds hold wide words (narrowed at the write-back)
+template <class F, class = void>
+struct is_wide : std::false_type {};
+template <class F>
+struct is_wide<F, std::enable_if_t<F::kWide>> : std::true_type {};
 
 struct F62 {
     using W = uint64_t;
