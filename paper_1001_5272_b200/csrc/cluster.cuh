@@ -781,12 +781,16 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_last_inv(LaunchArgs<F> 
     const int64_t o = a.xd.o(v) + (int64_t)K * C;
     W* x = a.x + o;
     const W* st = a.stash + (v - a.vbase) * (int64_t)C;
+    TFTB_TAIL_STAMP(a, 8);
     tile_load<W>(S, x, h, C, [&](uint32_t i, W w) { return i < h ? w : st[i]; });
     __syncthreads();
+    TFTB_TAIL_STAMP(a, 9);
     const TwBig<F> tpf{a.R.Zf, a.R.Zfh, K, CL, a.R.zb, f}, tpi{a.R.Zi, a.R.Zih, K, CL, a.R.zb, f};
     SmemTile<W> tl{S, CL, 0};
     itft_phases23<0>(f, tl, h, tpf, tpi, a.R);
+    TFTB_TAIL_STAMP(a, 10);
     tile_store<W>(x, S, h, [&](W w) { return f.canon(w); });
+    TFTB_TAIL_STAMP(a, 11);
 }
 
 // ================================================ two-pass plan, column pass
@@ -984,6 +988,47 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
             if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
         }
     }
+}
+
+// Inverse step 2 for vectors whose last chunk is nearly full (few columns
+// c >= h, e.g. n = 2^k - 1): one CTA per such column instead of one per
+// 2^WLOG-column tile.  A lone tile CTA transforms 2^col_tile_log words to
+// solve a handful of columns while the GPU waits for it (the steps after it
+// are serial: single 2^25 - 1-word vector, 77 us); a column CTA transforms
+// 2^L0.  Same arithmetic as k_colc_inv(which = 0) on that column.
+// grid: (C - h, vectors), uniform lengths only (dispatch.cuh)
+template <class F, int L0>
+__global__ void __launch_bounds__(256) k_col1_inv(LaunchArgs<F> a) {
+    using W = typename F::W;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    W* S = reinterpret_cast<W*>(smem_raw);
+    const int64_t v = a.vbase + blockIdx.y;
+    const int64_t n = a.xd.n(v);
+    const int l1 = a.l1;
+    if (ceil_lg_dev(n) - l1 != L0) return;
+    const uint32_t C = 1u << l1;
+    const uint32_t K = (uint32_t)(n >> l1), h = (uint32_t)(n & (C - 1));
+    const uint32_t c = h + blockIdx.x;
+    if (!h || c >= C) return;
+    const F f = a.f;
+    W* x = a.x + a.xd.o(v) + c;
+    TFTB_TAIL_STAMP(a, 0);
+    for (uint32_t r = threadIdx.x; r < (1u << L0); r += blockDim.x) S[r + (r >> 5)] = r < K ? x[(size_t)r * C] : W(0);
+    __syncthreads();
+    TFTB_TAIL_STAMP(a, 1);
+    const TwPrefix<F> tpf{a.R.Zf}, tpi{a.R.Zi};
+    inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, 0>(f, S, tpi, a.R.ipow2, K);
+    TFTB_TAIL_STAMP(a, 2);
+    SmemTile<W> tl{S, L0, 0};
+    itft_phases23<0>(f, tl, K, tpf, tpi, a.R);
+    TFTB_TAIL_STAMP(a, 3);
+    for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) x[(size_t)r * C] = f.canon(S[r + (r >> 5)]);
+    W* red = S + padded_words(1u << L0);
+    W* nv = red + blockDim.x;
+    TFTB_TAIL_STAMP(a, 4);
+    colsum_pow(f, tl, K, omega_w(f, a.R, K), a.R.oneW, red, nv);
+    if (threadIdx.x == 0) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[0];
+    TFTB_TAIL_STAMP(a, 5);
 }
 
 // ============================ forward for 2^CL < n <= 8 2^CL, no DSMEM

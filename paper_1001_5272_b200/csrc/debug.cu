@@ -96,3 +96,11 @@ extern "C" int tftb_debug_cluster_timing(uint64_t p, uint64_t top, int K, void* 
     CK(cudaDeviceSynchronize());
     return 0;
 }
+
+// Device buffer (16 x u64) that receives the phase stamps of the large
+// inverse's single-CTA tail kernels (k_col1_inv 0..5, k_last_inv 8..11) on
+// later executions; null switches them off.
+extern "C" int tftb_debug_tail_timing(unsigned long long* out) {
+    tftb::g_tail_timing = out;
+    return 0;
+}

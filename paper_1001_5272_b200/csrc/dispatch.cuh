@@ -121,7 +121,7 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
 template <class F>
 int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, const typename F::W* pre,
               int64_t count, VecDesc<typename F::W> xd, VecDesc<typename F::W> ind, int64_t maxn,
-              bool inverse, cudaStream_t st, typename F::W* stash_buf = nullptr) {
+              bool inverse, cudaStream_t st, typename F::W* stash_buf = nullptr, int64_t uni_n = 0) {
     using W = typename F::W;
     Plan pl;
     if (make_plan<F>(maxn, &pl)) return -1;
@@ -133,6 +133,7 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     a.in = in ? in : x;
     a.ind = in ? ind : xd;
     a.pre = pre;
+    a.timing = g_tail_timing;  // debug: stamps of the large inverse's tail kernels (null in production)
     static const int dense_cols = getenv("TFTB_DENSE_COLS") != nullptr;  // A/B knob
     a.dense_cols = dense_cols;
     a.l0 = pl.l0;
@@ -232,17 +233,27 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     // compile-time column kernels, one instantiation per l0
     void (*colf)(LaunchArgs<F>) = nullptr;
     void (*coli)(LaunchArgs<F>, int) = nullptr;
+    void (*col1)(LaunchArgs<F>) = nullptr;  // per-column step 2 (long columns only)
     switch (pl.l0) {
-#define TFTB_COL(L)                     \
-    case L:                             \
-        colf = k_colc_fwd<F, L>;        \
-        coli = k_colc_inv<F, L>;        \
+#define TFTB_COL(L)                                   \
+    case L:                                           \
+        colf = k_colc_fwd<F, L>;                      \
+        coli = k_colc_inv<F, L>;                      \
+        if constexpr (L >= 8) col1 = k_col1_inv<F, L>; \
         break;
         TFTB_COL(4) TFTB_COL(5) TFTB_COL(6) TFTB_COL(7) TFTB_COL(8) TFTB_COL(9)
         TFTB_COL(10) TFTB_COL(11) TFTB_COL(12) TFTB_COL(13) TFTB_COL(14)
 #undef TFTB_COL
         default: return fail("no column kernel for this plan");
     }
+    // Step 2 of the inverse by column when the batch has few columns c >= h
+    // (uniform lengths with a nearly full last chunk): at most two CTAs per SM
+    static const bool no_col1 = getenv("TFTB_NO_COL1") != nullptr;  // A/B knob
+    const uint32_t h_uni = uni_n ? (uint32_t)(uni_n & (C - 1)) : 0;
+    const int64_t cols2 = h_uni ? (int64_t)(C - h_uni) : 0;
+    const size_t sm_col1 = (padded_words(1u << pl.l0) + kNT + 8) * sizeof(W);
+    const bool narrow = inverse && col1 && !no_col1 && cols2 > 0 && cols2 * count <= 296;
+    if (narrow && set_smem(col1, sm_col1)) return -1;
     if (pl.wlog != std::max(0, std::min(10, Limits<F>::col_t - pl.l0))) return fail("column plan mismatch");
     if (set_smem(colf, sm_col) || set_smem(coli, sm_col)) return -1;
     // chunk kernels for this plan's chunk size (2^CL, or 2^14 for the u64 words
@@ -262,7 +273,8 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
                 g_launches += 2;
             } else {
                 k_chunk_inv<F, CLK><<<gchunk, kNT, sm_chunk, st>>>(a);
-                coli<<<gcol, kNT, sm_col, st>>>(a, 0);
+                if (narrow) col1<<<dim3((unsigned)cols2, nv), kNT, sm_col1, st>>>(a);
+                else coli<<<gcol, kNT, sm_col, st>>>(a, 0);
                 k_last_inv<F, CLK><<<glast, kNT, sm_chunk, st>>>(a);
                 coli<<<gcol, kNT, sm_col, st>>>(a, 1);
                 g_launches += 4;
@@ -376,6 +388,9 @@ int plan_create(const RingHost* rh, int64_t count, int64_t n, int64_t stride, co
             len[i] = h_len ? h_len[v] : n;
             g.maxn = std::max(g.maxn, len[i]);
         }
+        g.uni_n = g.maxn;
+        for (int64_t i = 0; i < g.count; i++)
+            if (len[i] != g.maxn) g.uni_n = 0;
         Plan pl;
         make_plan<F>(g.maxn, &pl);
         if (pl.kind == kLarge || pl.kind == kP2R)  // (p2r: its 2^k prefix runs the two-pass plan;
@@ -440,7 +455,7 @@ int plan_exec(const PlanImpl* P, void* data, int inverse, const void* pre, cudaS
             CK(cudaStreamWaitEvent(gs, P->ev_fork, 0));
         }
         rc = run_group<F>(P->rh, (W*)data, nullptr, (const W*)pre, g.count, xd, xd, g.maxn, inverse != 0, gs,
-                          (W*)P->stash);
+                          (W*)P->stash, g.uni_n);
         if (P->fork) CK(cudaEventRecord(P->ev_join[i], gs));
     }
     if (P->fork)
@@ -460,7 +475,7 @@ int run_batch(const RingHost* rh, void* data, const void* in, int64_t count, int
     if (!h_off && !h_len) {
         VecDesc<W> xd{nullptr, nullptr, stride, n};
         VecDesc<W> ind{nullptr, nullptr, in_stride, in_n};
-        return run_group<F>(rh, (W*)data, (const W*)in_data, (const W*)pre, count, xd, ind, n, inverse, st);
+        return run_group<F>(rh, (W*)data, (const W*)in_data, (const W*)pre, count, xd, ind, n, inverse, st, nullptr, n);
     }
     (void)in;
     PlanImpl P;

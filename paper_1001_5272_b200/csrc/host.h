@@ -24,6 +24,7 @@ typedef unsigned __int128 u128;
 
 extern thread_local std::string g_err;
 extern thread_local int64_t g_launches;
+extern unsigned long long* g_tail_timing;  // debug (debug.cu tftb_debug_tail_timing); null in production
 // device bytes a transform allocates beyond its own n words (stash, p2r
 // partials, the product's second operand): current and high-water mark of
 // this thread's calls -- the footprint audit (tftb_aux_bytes)
@@ -223,6 +224,7 @@ struct Scratch {
 
 struct PlanGroup {
     int64_t count, maxn;
+    int64_t uni_n = 0;  // the common length when every vector of the group has the same, else 0
     size_t arr_off;  // offsets then lengths, in darr
 };
 

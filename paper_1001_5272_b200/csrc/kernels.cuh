@@ -69,6 +69,14 @@ __device__ __forceinline__ unsigned long long gtime() {
         }                                                                                                  \
     } while (0)
 
+// Stamps of the single-CTA tail kernels of a large inverse (k_col1_inv,
+// k_last_inv): run-time guarded -- these kernels are latency chains of one
+// CTA, the guard costs them nothing (timing is null in production)
+#define TFTB_TAIL_STAMP(a, k)                                                                     \
+    do {                                                                                          \
+        if ((a).timing && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) (a).timing[k] = gtime(); \
+    } while (0)
+
 // Hint: bring words [p, p + words) into L2 with TMA bulk prefetches (the
 // copy engine streams them while the SM works).  Only the 16-byte-aligned
 // inner span, so it never touches bytes outside the range.

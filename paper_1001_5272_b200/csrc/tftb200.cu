@@ -22,6 +22,7 @@ namespace tftb {
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+unsigned long long* g_tail_timing = nullptr;
 thread_local int64_t g_aux_cur = 0, g_aux_peak = 0;
 thread_local int64_t g_stage_cur = 0, g_stage_peak = 0;
 
@@ -185,6 +186,44 @@ int build_tables(RingHost* rh, RingDev<W>* out) {
     return 0;
 }
 
+// F32W's difference (field.cuh) reads the carry flag sub.cc leaves behind with
+// an addc, which relies on how this toolchain encodes a borrow.  Checked once
+// per process on the device, so a different convention fails loudly at ring
+// creation instead of giving wrong residues.
+__global__ void k_f32w_probe(F32 f0, unsigned* bad) {
+    const F32W f(f0);
+    const uint32_t p = f.p;
+    const uint32_t as[] = {0u, 1u, p - 1, p, p + 1, 0xFFFFFFFFu, 0x80000000u, 1073741823u, 1073741824u};
+    const uint32_t bs[] = {0u, 1u, p - 1, p >> 1, 1073741824u, 2147483648u};
+    unsigned n = 0;
+    for (uint32_t a : as)
+        for (uint32_t b : bs) {
+            const uint64_t ar = a % p;
+            if (f.addw(a, b) % p != (ar + b) % p) ++n;
+            if (f.subw(a, b) % p != (ar + p - b) % p) ++n;
+        }
+    *bad = n;
+}
+int f32w_probe(uint64_t p) {
+    static std::map<std::pair<int, uint64_t>, bool> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (done[{dev, p}]) return 0;
+    F32 f{};
+    f.p = (uint32_t)p;
+    f.pinv = inv_word<uint32_t>((uint32_t)p);
+    unsigned* d = nullptr;
+    unsigned h = 1;
+    CK(cudaMalloc(&d, sizeof(unsigned)));
+    k_f32w_probe<<<1, 1>>>(f, d);
+    cudaError_t e = cudaMemcpy(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(std::string("F32W probe: ") + cudaGetErrorString(e));
+    if (h) return fail("F32W carry-flag probe failed: rebuild field.cuh's subw for this toolchain");
+    done[{dev, p}] = true;
+    return 0;
+}
+
 std::mutex g_ring_mu;
 std::map<std::tuple<uint64_t, uint64_t, int, int>, std::unique_ptr<RingHost>> g_rings;
 
@@ -218,11 +257,13 @@ int get_ring(uint64_t p, uint64_t top, int K, RingHost** out) {
     rh->wbytes = p < (1ull << 32) ? 4 : 8;
     rh->kind = p < (1ull << 30) ? 0 : (p < (1ull << 32) ? 1 : 2);
     int km1 = K > 0 ? K - 1 : 0;
-    rh->zb = std::min(km1, 16);
+    static const int zb_max = getenv("TFTB_ZB") ? atoi(getenv("TFTB_ZB")) : 16;  // A/B knob
+    rh->zb = std::min(km1, zb_max);
     rh->zh = std::min(km1 - rh->zb, 16);
     int rc = rh->wbytes == 4 ? build_tables<uint32_t>(rh.get(), &rh->r32)
                              : build_tables<uint64_t>(rh.get(), &rh->r64);
     if (rc) return rc;
+    if (rh->kind == 1 && (rc = f32w_probe(p))) return rc;
     *out = rh.get();
     g_rings[key] = std::move(rh);
     return 0;

@@ -519,3 +519,30 @@ def test_host_api_device_memory_is_the_ring_words_plus_bounded_staging():
     r = out.size
     assert backend.stage_bytes() <= 4 * (a.size + b.size + 2 * r) + 8 * min(r, 1 << 22) + 512
     assert int(out[0]) == int(a[0]) * int(b[0]) % cfg.p
+
+
+def test_nearly_full_last_chunk_inverse(golden):
+    """Vectors whose last chunk is nearly full (few columns c >= h) solve
+    those columns one per CTA (k_col1_inv): the inverse against the oracle
+    at 2^22 - j, and exact round trips of uniform batches and of longer
+    vectors on all three word types (the forward is pinned elsewhere)."""
+    cfg = T.default_config()
+    for n in ((1 << 22) - 1, (1 << 22) - 37):
+        z = gen(n + 5, cfg.p, n)
+        assert np.array_equal(run(T.itft, z, cfg), O.itft(z, cfg.p, cfg.omegaK, cfg.K)), n
+    cases = [("p998244353", (1 << 23) - 3, 1), ("p998244353", (3 << 21) - 2, 2), ("p998244353", (1 << 22) - 140, 2),
+             ("p3221225473", (1 << 24) - 1, 1), ("p3221225473", (5 << 22) - 296, 1),
+             ("p4179340454199820289", (1 << 22) - 1, 1), ("p4179340454199820289", (1 << 23) - 9, 2)]
+    for key, n, count in cases:
+        c = cfg_for(golden, key)
+        flat = gen(n + count, c.p, n * count)
+        d = device.to_words(flat, c)
+        o = d.clone()
+        device.tft_batch_(d, c, n=n, count=count)
+        assert not torch.equal(d, o)
+        device.tft_batch_(d, c, n=n, count=count, inverse=True)
+        assert torch.equal(d, o), (key, n, count)
+        plan = device.BatchPlan(c, [n] * count)
+        plan.execute(d)
+        plan.execute(d, inverse=True)
+        assert torch.equal(d, o), (key, n, count, "plan")
