@@ -218,8 +218,10 @@ struct F32W : F32 {
         x = addw(a, b);
         y = subw(a, b);
     }
-    TFT_DEV void inv(W& x, W& y, Tw<W> t) const {
-        const W a = x, b = narrow(y);
+    // ycanon: y is known canonical (a tile word, or the product side of the
+    // layer below -- a compile-time fact after unrolling, tile.cuh reg_inv)
+    TFT_DEV void inv(W& x, W& y, Tw<W> t, bool ycanon = false) const {
+        const W a = x, b = ycanon ? y : narrow(y);
         x = addw(a, b);
         y = mulw(subw(a, b), t);
     }

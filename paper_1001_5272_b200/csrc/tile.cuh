@@ -149,7 +149,15 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
             const int i = (q << (ST + 1)) | r;
             const uint32_t pos = base + ((uint32_t)i << slo);
             if (MASK && pos >= hs) continue;
-            f.inv(v[i], v[i | (1 << ST)], t);
+            if constexpr (is_wide<F>::value) {
+                // the upper word is canonical when it comes from the tile
+                // (first layer) or was the product side of the layer below
+                // (bit ST-1 of its index; an active pair's sub-blocks were
+                // active below, masked or not)
+                f.inv(v[i], v[i | (1 << ST)], t, ST == 0 || ((r >> (ST > 0 ? ST - 1 : 0)) & 1));
+            } else {
+                f.inv(v[i], v[i | (1 << ST)], t);
+            }
             if (MASK ? pos >= hs1 : scale_all) {
                 v[i] = f.scale(v[i], sc);
                 v[i | (1 << ST)] = f.scale(v[i | (1 << ST)], sc);
@@ -180,7 +188,7 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                       bool uniform = false) {
     using W = typename F::W;
     const int t = tl.t;
-    const int wl = WL >= 0 ? WL : wl;
+    const int wl = WL >= 0 ? WL : tl.wlog;
     const uint32_t ncols = 1u << wl;
     auto at = [&](uint32_t pos, uint32_t col) -> W& {
         const uint32_t idx = (pos << wl) | col;

@@ -172,15 +172,15 @@ int main() {
         f.pinv = x;
         Tw<uint32_t>* Z; uint32_t* ZM; Tw<uint32_t>* ip;
         tables(f, p, false, &Z, &ZM, &ip);
-        printf("== F32 forward\n");
-        run<F32, F32B, false, 0>("top  (shipped)", f, Z, ZM, out, ip);
-        run<F32, F32B, false, 1>("top  F32B", f, Z, ZM, out, ip);
-        run<F32, F32B, false, 3>("bot  (shipped)", f, Z, ZM, out, ip);
-        run<F32, F32B, false, 4>("bot  F32B", f, Z, ZM, out, ip);
+        printf("== F32 forward (canonical = the field outside the rounds; wide = F32W, what the rounds run)\n");
+        run<F32, F32W, false, 0>("top  canonical", f, Z, ZM, out, ip);
+        run<F32, F32W, false, 1>("top  wide (shipped)", f, Z, ZM, out, ip);
+        run<F32, F32B, false, 4>("bot  canonical", f, Z, ZM, out, ip);
+        run<F32, F32W, false, 3>("bot  wide (shipped)", f, Z, ZM, out, ip);
         printf("== F32 inverse\n");
-        run<F32, F32B, true, 0>("top  (shipped)", f, Z, ZM, out, ip);
-        run<F32, F32B, true, 1>("top  F32B", f, Z, ZM, out, ip);
-        run<F32, F32B, true, 3>("bot  (shipped)", f, Z, ZM, out, ip);
-        run<F32, F32B, true, 4>("bot  F32B", f, Z, ZM, out, ip);
+        run<F32, F32W, true, 0>("top  canonical", f, Z, ZM, out, ip);
+        run<F32, F32W, true, 1>("top  wide (shipped)", f, Z, ZM, out, ip);
+        run<F32, F32B, true, 4>("bot  canonical", f, Z, ZM, out, ip);
+        run<F32, F32W, true, 3>("bot  wide (shipped)", f, Z, ZM, out, ip);
     }
 }
