@@ -275,9 +275,15 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
                 k_chunk_inv<F, CLK><<<gchunk, kNT, sm_chunk, st>>>(a);
                 if (narrow) col1<<<dim3((unsigned)cols2, nv), kNT, sm_col1, st>>>(a);
                 else coli<<<gcol, kNT, sm_col, st>>>(a, 0);
-                k_last_inv<F, CLK><<<glast, kNT, sm_chunk, st>>>(a);
-                coli<<<gcol, kNT, sm_col, st>>>(a, 1);
-                g_launches += 4;
+                g_launches += 2;
+                // uniform lengths that are whole chunks (2^k, 3 2^k, a p2r
+                // prefix) have no partial chunk: steps 3 and 4 would be two
+                // empty launches (~8 us of a single vector's inverse)
+                if (!(uni_n && !h_uni)) {
+                    k_last_inv<F, CLK><<<glast, kNT, sm_chunk, st>>>(a);
+                    coli<<<gcol, kNT, sm_col, st>>>(a, 1);
+                    g_launches += 2;
+                }
             }
             CK(cudaGetLastError());
         }
@@ -323,9 +329,9 @@ int run_p2r(const RingHost* rh, LaunchArgs<F> a, int k, int r, int64_t count, Ve
     };
     if (!inverse) {
         if (launch(false)) return -1;
-        return run_group<F>(rh, a.x, nullptr, nullptr, count, pre_d, pre_d, H, false, st, stash_buf);
+        return run_group<F>(rh, a.x, nullptr, nullptr, count, pre_d, pre_d, H, false, st, stash_buf, H);
     }
-    if (run_group<F>(rh, a.x, nullptr, a.pre, count, pre_d, pre_d, H, true, st, stash_buf)) return -1;
+    if (run_group<F>(rh, a.x, nullptr, a.pre, count, pre_d, pre_d, H, true, st, stash_buf, H)) return -1;
     // V[s][t] = rho_s^t, rho_s = omega_{2^k + s}: its inverse on the host
     {
         const uint64_t p = rh->p;
