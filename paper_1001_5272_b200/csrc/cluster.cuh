@@ -215,7 +215,7 @@ TFT_DEV constexpr uint32_t unit_off(int i) {
 
 // Forward round.  With PRUNE, units whose every output row is >= lim are
 // skipped (only rows < lim are needed after the remaining stages).
-template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
+template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, int ZT = 0, class TP>
 TFT_DEV void fwd_round_units(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
     using W = typename F::W;
     constexpr uint32_t NU = 1u << (TL - KK + WLOG);
@@ -228,8 +228,9 @@ TFT_DEV void fwd_round_units(const F& f, typename F::W* S, const TP& tp, uint32_
         W* pb = S + idx0 + (idx0 >> 5);
         W v[1 << KK];
 #pragma unroll
-        for (int i = 0; i < (1 << KK); ++i) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];
-        reg_fwd<F, KK, KK - 1>(f, v, base, SLO, tp);
+        for (int i = 0; i < (1 << KK); ++i)
+            if (ZT == 0 || !((i >> (KK - 1)) & 1)) v[i] = pb[unit_off<SLO, WLOG, KK>(i)];  // (zero rows: not read)
+        reg_fwd<F, KK, KK - 1, ZT>(f, v, base, SLO, tp);
         if constexpr (is_wide<F>::value) {
 #pragma unroll
             for (int i = 0; i < (1 << KK); ++i) v[i] = f.narrow(v[i]);
@@ -314,14 +315,14 @@ TFT_DEV auto round_field(const F& f) {
     else return f;
 }
 
-template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, class TP>
+template <class F, int TL, int KK, int SLO, int WLOG, bool PRUNE, int ZT = 0, class TP>
 TFT_DEV void fwd_round_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need, Lanes ln) {
     if constexpr (SLO == 0 && WLOG == 0 && bottom_words<F, TP>()) {
         const auto fb = bottom_field(f);
-        fwd_round_units<decltype(fb), TL, KK, SLO, WLOG, PRUNE>(fb, S, tp.mont(), need, ln);
+        fwd_round_units<decltype(fb), TL, KK, SLO, WLOG, PRUNE, ZT>(fb, S, tp.mont(), need, ln);
     } else {
         const auto fr = round_field(f);
-        fwd_round_units<decltype(fr), TL, KK, SLO, WLOG, PRUNE>(fr, S, tp, need, ln);
+        fwd_round_units<decltype(fr), TL, KK, SLO, WLOG, PRUNE, ZT>(fr, S, tp, need, ln);
     }
 }
 
@@ -339,14 +340,16 @@ TFT_DEV void inv_round_ct(const F& f, typename F::W* S, const TP& tp, const Tw<t
 
 // stages [0, SHI): one round of min(5, SHI-5) stages from the top (s_lo >= 5),
 // recursing down to a final 5-or-fewer-stage round at s_lo = 0.
-template <class F, int TL, int SHI, int WLOG = 0, bool PRUNE = false, class TP>
+// ZT (first call only, SHI = TL): rows >= 2^(TL-ZT) of the tile are zero on
+// entry; the top round's first ZT layers are copies (clamped to that round).
+template <class F, int TL, int SHI, int WLOG = 0, bool PRUNE = false, int ZT = 0, class TP>
 TFT_DEV void fwd_rounds_ct(const F& f, typename F::W* S, const TP& tp, uint32_t need = 0, Lanes ln = cta_lanes()) {
     if constexpr (SHI <= 5) {
-        fwd_round_ct<F, TL, SHI, 0, WLOG, PRUNE>(f, S, tp, need, ln);
+        fwd_round_ct<F, TL, SHI, 0, WLOG, PRUNE, (ZT < SHI ? ZT : SHI)>(f, S, tp, need, ln);
         __syncthreads();
     } else {
         constexpr int KK = (SHI - 5) >= 5 ? 5 : (SHI - 5);
-        fwd_round_ct<F, TL, KK, SHI - KK, WLOG, PRUNE>(f, S, tp, need, ln);
+        fwd_round_ct<F, TL, KK, SHI - KK, WLOG, PRUNE, (ZT < KK ? ZT : KK)>(f, S, tp, need, ln);
         __syncthreads();
         fwd_rounds_ct<F, TL, SHI - KK, WLOG, PRUNE>(f, S, tp, need, ln);
     }
@@ -910,7 +913,9 @@ TFT_DEV void col_store(const F& f, typename F::W* xt, const typename F::W* S, ui
     }
 }
 
-template <class F, int L0>
+// ZT: the input's rows >= 2^(L0-ZT) are zero padding in every column (a
+// product's operand, ceil(nin / C) <= 2^(L0-ZT), checked by the host)
+template <class F, int L0, int ZT = 0>
 __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
     using W = typename F::W;
     constexpr int WLOG = col_wlog<F, L0>();
@@ -928,7 +933,7 @@ __global__ void __launch_bounds__(256) k_colc_fwd(LaunchArgs<F> a) {
     col_load<W, L0, WLOG>(S, in + c0, C, nin - c0, [](uint32_t, uint32_t, W w) { return w; });
     __syncthreads();
     // rows <= K are the only outputs (row K: real for c < h, the stash for c >= h)
-    fwd_rounds_ct<F, L0, L0, WLOG, true>(f, S, TwPrefix<F>{a.R.Zf}, K + (h ? 1u : 0u));
+    fwd_rounds_ct<F, L0, L0, WLOG, true, ZT>(f, S, TwPrefix<F>{a.R.Zf}, K + (h ? 1u : 0u));
     const uint32_t NC = 1u << WLOG;
     // complete rows r < K, then row K: real words for c < h, the stash for c >= h
     col_store<F, WLOG>(f, x + c0, S, C, 0, min(K, 1u << L0), 0, NC);

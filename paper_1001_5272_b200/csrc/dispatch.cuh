@@ -231,6 +231,14 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
     const size_t sm_col = (padded_words(1u << (pl.l0 + pl.wlog)) + kNT + (1u << pl.wlog) + 8) * sizeof(W);
     const size_t sm_chunk = padded_words(C) * sizeof(W);
     // compile-time column kernels, one instantiation per l0
+    // forward of a zero-padded operand (a product's A or B, uniform input
+    // length): the column networks' top zt <= 2 layers see zero upper rows
+    static const bool no_zt = getenv("TFTB_NO_ZT") != nullptr;  // A/B knob
+    int zt = 0;
+    if (!inverse && in && in != x && !ind.len && !no_zt) {
+        const int64_t rows_in = (ind.n0 + C - 1) / C;
+        while (zt < 2 && pl.l0 - zt - 1 >= 0 && rows_in <= (1ll << (pl.l0 - zt - 1))) ++zt;
+    }
     void (*colf)(LaunchArgs<F>) = nullptr;
     void (*coli)(LaunchArgs<F>, int) = nullptr;
     void (*col1)(LaunchArgs<F>) = nullptr;  // per-column step 2 (long columns only)
@@ -238,6 +246,10 @@ int run_group(const RingHost* rh, typename F::W* x, const typename F::W* in, con
 #define TFTB_COL(L)                                   \
     case L:                                           \
         colf = k_colc_fwd<F, L>;                      \
+        if constexpr (L >= 6) {                       \
+            if (zt == 1) colf = k_colc_fwd<F, L, 1>;  \
+            if (zt == 2) colf = k_colc_fwd<F, L, 2>;  \
+        }                                             \
         coli = k_colc_inv<F, L>;                      \
         if constexpr (L >= 8) col1 = k_col1_inv<F, L>; \
         break;

@@ -108,23 +108,35 @@ struct TwPrefix {  // untwisted tile: theta(s, J) = Z[J]
 // s = slo + ST) pairs (i, i + 2^ST) with twiddle index (base >> (s+1)) + q,
 // q = i >> (ST+1).  Template recursion keeps every index a compile-time
 // constant so the unit stays in registers.
-template <class F, int KK, int ST, class TP>
+// ZT: the unit's top ZT layers have an all-zero upper input (the zero padding
+// of a product's operand, known to the host): (a + w 0, a - w 0) is a copy.
+template <class F, int KK, int ST, int ZT = 0, class TP>
 TFT_DEV void reg_fwd(const F& f, typename F::W* v, uint32_t base, int slo, const TP& tp) {
     using W = typename F::W;
     constexpr int NQ = 1 << (KK - 1 - ST);
     const int s = slo + ST;
-    Tw<W> w[NQ];
-    tp.template get_many<NQ>(s, base >> (s + 1), w);
+    if constexpr (ST >= KK - ZT) {
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const Tw<W> t = w[q];
+        for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int r = 0; r < (1 << ST); ++r) {
-            const int i = (q << (ST + 1)) | r;
-            f.fwd(v[i], v[i | (1 << ST)], t);
+            for (int r = 0; r < (1 << ST); ++r) {
+                const int i = (q << (ST + 1)) | r;
+                v[i | (1 << ST)] = v[i];
+            }
+    } else {
+        Tw<W> w[NQ];
+        tp.template get_many<NQ>(s, base >> (s + 1), w);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const Tw<W> t = w[q];
+#pragma unroll
+            for (int r = 0; r < (1 << ST); ++r) {
+                const int i = (q << (ST + 1)) | r;
+                f.fwd(v[i], v[i | (1 << ST)], t);
+            }
         }
     }
-    if constexpr (ST > 0) reg_fwd<F, KK, ST - 1>(f, v, base, slo, tp);
+    if constexpr (ST > 0) reg_fwd<F, KK, ST - 1, ZT>(f, v, base, slo, tp);
 }
 
 // ascending layers ST .. KK-1; pairs with pos >= lim[s] are skipped (MASK) and
