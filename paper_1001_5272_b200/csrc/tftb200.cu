@@ -547,7 +547,9 @@ int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64
     // sub-batches of ~total/48 words (at least 2^22, at most 2^25 words
     // unless one vector is longer): short pipeline fill and drain
     // (measured: 12 -> 48 parts, +2% e2e)
-    const int64_t target = std::min<int64_t>(std::max<int64_t>(total / 48, 1 << 22), 1 << 25);
+    static const int parts = getenv("TFTB_PIPE_PARTS") ? atoi(getenv("TFTB_PIPE_PARTS")) : 48;      // A/B knobs
+    static const int minlog = getenv("TFTB_PIPE_MINLOG") ? atoi(getenv("TFTB_PIPE_MINLOG")) : 22;
+    const int64_t target = std::min<int64_t>(std::max<int64_t>(total / parts, 1ll << minlog), 1 << 25);
     std::vector<SubBatch> subs;
     int64_t maxw = 0;
     for (int64_t i0 = 0; i0 < count;) {
@@ -579,9 +581,13 @@ int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64
     CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     CK(cudaEventRecord(ready, ss[0]));
     for (int i = 1; i < kPipeStreams; i++) CK(cudaStreamWaitEvent(ss[i], ready, 0));
+    // Each sub-batch's plan is built as its turn comes, its arrays allocated
+    // and uploaded stream-ordered on the slot's stream: the host runs ahead
+    // of the copies instead of building all plans (an allocation and a
+    // blocking upload each) before the first transfer starts.
     std::vector<std::unique_ptr<PlanImpl>> plans;
     std::vector<int64_t> poff, plen;
-    for (auto& sb : subs) {
+    auto make = [&](const SubBatch& sb, cudaStream_t st) -> int {
         poff.clear();
         plen.clear();
         int64_t acc = 0;
@@ -593,12 +599,8 @@ int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64
         plans.emplace_back(new PlanImpl());
         // (no forking: the pipeline's slots already overlap sub-batches, and
         // per-plan side streams would cost a stream creation per sub-batch)
-        if (plan_create<F>(rh, sb.v1 - sb.v0, 0, 0, poff.data(), plen.data(), plans.back().get(), nullptr, false,
-                           false)) {
-            cudaEventDestroy(ready);
-            return -1;
-        }
-    }
+        return plan_create<F>(rh, sb.v1 - sb.v0, 0, 0, poff.data(), plen.data(), plans.back().get(), st, true, false);
+    };
     int rc = 0;
     for (size_t b = 0; b < subs.size() && !rc; b++) {
         const SubBatch& sb = subs[b];
@@ -609,6 +611,10 @@ int host_batch_pipeline(const RingHost* rh, uint64_t* x, const std::vector<int64
         for (auto& r : sb.runs) {
             if (cudaMemcpyAsync(d64 + at, x + r.first, (size_t)r.second * 8, cudaMemcpyHostToDevice, st)) rc = -1;
             at += r.second;
+        }
+        if (make(sb, st)) {
+            rc = -1;
+            break;
         }
         const int nb = (int)std::min<int64_t>((sb.words + 255) / 256, 148 * 8);
         if (narrow) {

@@ -1,5 +1,7 @@
-"""Small runs of the round-2 paths for compute-sanitizer (memcheck / racecheck):
-    compute-sanitizer --tool memcheck python tools/sanitize.py
+"""Small runs of the round-2 paths (a quick exercise script; written for
+compute-sanitizer, which is closed on this GPU pool, so it only checks the
+round trips):
+    python tools/sanitize.py
 F32 wide rounds, step 2 by column (n = 2^k - j), whole-chunk inverses, and a
 two-pass product whose operands are zero-padded (ZT column kernels)."""
 import os, sys
