@@ -546,3 +546,19 @@ def test_nearly_full_last_chunk_inverse(golden):
         plan.execute(d)
         plan.execute(d, inverse=True)
         assert torch.equal(d, o), (key, n, count, "plan")
+
+
+def test_two_pass_products_with_zero_padded_operands(golden):
+    """Two-pass products whose operands leave the column networks' top one
+    or two layers with zero upper rows (k_colc_fwd ZT = 0, 1, 2 in every
+    combination, operands much shorter and almost as long as the product),
+    on both u32 word types and u64, against the oracle's product."""
+    shapes = ((150000, 150001), (299990, 12), (5, 280000), (100000, 190000), (70000, 70000), (262144, 1))
+    for key in ("p998244353", "p3221225473", "p4179340454199820289"):
+        cfg = cfg_for(golden, key)
+        for la, lb in shapes[:3] if key != "p998244353" else shapes:
+            a = gen(la + 3, cfg.p, la)
+            b = gen(lb + 7, cfg.p, lb)
+            out = np.zeros(la + lb - 1, dtype=np.uint64)
+            T.multiply(a, b, out, cfg)
+            assert np.array_equal(out, O.multiply(a, b, cfg.p, cfg.omegaK, cfg.K)), (key, la, lb)
