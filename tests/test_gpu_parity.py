@@ -562,3 +562,24 @@ def test_two_pass_products_with_zero_padded_operands(golden):
             out = np.zeros(la + lb - 1, dtype=np.uint64)
             T.multiply(a, b, out, cfg)
             assert np.array_equal(out, O.multiply(a, b, cfg.p, cfg.omegaK, cfg.K)), (key, la, lb)
+
+
+def test_extreme_residues_against_oracle(golden):
+    """Inputs made of the extreme residues 0, 1, p - 1 and (p - 1) / 2 (all
+    equal, alternating, and one hot) push the lazy and wide words of the
+    rounds to the ends of their ranges -- for p = 3221225473 the carries of
+    the 32-bit sums.  Tile, cluster and two-pass plans, forward and inverse,
+    on the three word types, against the oracle."""
+    for key in ("p998244353", "p3221225473", "p4179340454199820289"):
+        cfg = cfg_for(golden, key)
+        p = cfg.p
+        for n in (999, 16385, 40000, 150001):
+            pats = [np.full(n, p - 1, dtype=np.uint64),
+                    np.where(np.arange(n) % 2 == 0, p - 1, 0).astype(np.uint64),
+                    np.where(np.arange(n) % 3 == 0, (p - 1) // 2, p - 1).astype(np.uint64),
+                    np.concatenate([np.zeros(n - 1, dtype=np.uint64), np.array([p - 1], dtype=np.uint64)]),
+                    np.ones(n, dtype=np.uint64)]
+            for i, x in enumerate(pats):
+                y = run(T.tft, x, cfg)
+                assert np.array_equal(y, O.tft(x, p, cfg.omegaK, cfg.K)), (key, n, i)
+                assert np.array_equal(run(T.itft, x, cfg), O.itft(x, p, cfg.omegaK, cfg.K)), (key, n, i, "inv")
