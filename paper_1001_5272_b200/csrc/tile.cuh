@@ -156,11 +156,14 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const Tw<W> t = w[q];
+        // hs and hs1 are multiples of the pair group's span 2^(s+1), so the
+        // group's 2^ST pairs lie on one side of each: one test per group
+        const uint32_t posq = base + ((uint32_t)(q << (ST + 1)) << slo);
+        if (MASK && posq >= hs) continue;
+        const bool scl = MASK ? posq >= hs1 : scale_all;
 #pragma unroll
         for (int r = 0; r < (1 << ST); ++r) {
             const int i = (q << (ST + 1)) | r;
-            const uint32_t pos = base + ((uint32_t)i << slo);
-            if (MASK && pos >= hs) continue;
             if constexpr (is_wide<F>::value) {
                 // the upper word is canonical when it comes from the tile
                 // (first layer) or was the product side of the layer below
@@ -170,7 +173,7 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
             } else {
                 f.inv(v[i], v[i | (1 << ST)], t);
             }
-            if (MASK ? pos >= hs1 : scale_all) {
+            if (scl) {
                 v[i] = f.scale(v[i], sc);
                 v[i | (1 << ST)] = f.scale(v[i | (1 << ST)], sc);
             }
