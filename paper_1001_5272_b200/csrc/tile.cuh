@@ -204,11 +204,6 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
     using W = typename F::W;
     const int t = tl.t;
     const int wl = WL >= 0 ? WL : tl.wlog;
-    const uint32_t ncols = 1u << wl;
-    auto at = [&](uint32_t pos, uint32_t col) -> W& {
-        const uint32_t idx = (pos << wl) | col;
-        return tl.S[idx + (idx >> 5)];
-    };
     // uniform: every tile of the CTA walks all levels (the barriers must
     // match); tiles with nothing to do at a level just skip its work
     const bool act = h != 0 && h < (1u << t);
@@ -240,6 +235,24 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
     }
     Tw<W> wn = !pre && act && t >= dact ? tw2(t) : Tw<W>{};
     Tw<W> wn3 = !pre && act && dact <= t ? tw3(dact) : Tw<W>{};
+    // One level's sweep over the element pairs (lo, hi) = (idx, idx + Hw) for
+    // idx in [base_idx, base_idx + cnt): rows and columns are one flat index
+    // ((pos << wl) | col), so a lane walks it with a constant stride; the
+    // padded address of idx + 32 k is that of idx plus 33 k, which makes the
+    // stride and (for Hw a multiple of 32) the partner offset constants.
+    auto sweep = [&](uint32_t base_idx, uint32_t cnt, uint32_t Hw, auto body) {
+        if ((ln.n & 31) == 0 && (Hw & 31) == 0) {
+            const uint32_t i0 = base_idx + ln.id;
+            W* p = tl.S + i0 + (i0 >> 5);
+            const uint32_t off = Hw + (Hw >> 5), step = ln.n + (ln.n >> 5);
+            for (uint32_t g = ln.id; g < cnt; g += ln.n, p += step) body(p[0], p[off]);
+        } else {
+            for (uint32_t g = ln.id; g < cnt; g += ln.n) {
+                const uint32_t ia = base_idx + g, ib = ia + Hw;
+                body(tl.S[ia + (ia >> 5)], tl.S[ib + (ib >> 5)]);
+            }
+        }
+    };
     for (int d = t; d >= dlo; --d) {
         const Tw<W> w = pre ? pre2[d] : wn;
         if (!pre && act && d - 1 >= dact) wn = tw2(d - 1);
@@ -247,32 +260,25 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
             if (hd >= H) {
-                const uint32_t i0 = hd - H, cnt = (H - i0) << wl;
-                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = i0 + (g >> wl);
-                    W tv = at(B + H + i, col);
+                const uint32_t i0 = hd - H;
+                sweep((B + i0) << wl, (H - i0) << wl, H << wl, [&](W& lo, W& hi) {
                     if constexpr (F::kLazy) {  // values stay in [0, 4p)
-                        const W m = f.mulw(tv, w);
-                        const W x = f.red2(at(B + i, col)) - m + f.p2;
-                        at(B + i, col) = x;
-                        at(B + H + i, col) = f.red2(x) - m + f.p2;
+                        const W m = f.mulw(hi, w);
+                        const W x = f.red2(lo) - m + f.p2;
+                        lo = x;
+                        hi = f.red2(x) - m + f.p2;
                     } else {
-                        W lo = f.canon(at(B + i, col));
-                        W m = f.cmulw(tv, w);
-                        W x = f.csub(lo, m);
-                        at(B + i, col) = x;
-                        at(B + H + i, col) = f.csub(x, m);
+                        const W m = f.cmulw(hi, w);
+                        const W x = f.csub(f.canon(lo), m);
+                        lo = x;
+                        hi = f.csub(x, m);
                     }
-                }
+                });
             } else {
-                const uint32_t cnt = (H - hd) << wl;
-                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = hd + (g >> wl);
-                    W a = at(B + i, col);
-                    W b = at(B + H + i, col);
-                    if constexpr (F::kLazy) at(B + i, col) = f.red2(a) + f.mulw(b, w);
-                    else at(B + i, col) = f.cadd(a, f.cmulw(b, w));
-                }
+                sweep((B + hd) << wl, (H - hd) << wl, H << wl, [&](W& lo, W& hi) {
+                    if constexpr (F::kLazy) lo = f.red2(lo) + f.mulw(hi, w);
+                    else lo = f.cadd(lo, f.cmulw(hi, w));
+                });
             }
         }
         __syncthreads();
@@ -286,29 +292,22 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             if (hd >= H) {
                 const uint32_t cnt = (hd - H) << wl;
                 const Tw<W> wh = cnt ? f.tw(f.twmul(w, R.inv2)) : w;  // w / 2: one product per element
-                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = g >> wl;
+                sweep(B << wl, cnt, H << wl, [&](W& lo, W& hi) {
                     if constexpr (F::kLazy) {
-                        const W lo = f.red2(at(B + i, col));
-                        const W hi = f.red2(at(B + H + i, col));
-                        at(B + i, col) = f.mulw(lo + hi, R.inv2);
-                        at(B + H + i, col) = f.mulw(lo - hi + f.p2, wh);
+                        const W l = f.red2(lo), u = f.red2(hi);
+                        lo = f.mulw(l + u, R.inv2);
+                        hi = f.mulw(l - u + f.p2, wh);
                     } else {
-                        W lo = f.canon(at(B + i, col));
-                        W hi = at(B + H + i, col);
-                        at(B + i, col) = f.cmulw(f.cadd(lo, hi), R.inv2);
-                        at(B + H + i, col) = f.cmulw(f.csub(lo, hi), wh);
+                        const W l = f.canon(lo), u = hi;
+                        lo = f.cmulw(f.cadd(l, u), R.inv2);
+                        hi = f.cmulw(f.csub(l, u), wh);
                     }
-                }
+                });
             } else {
-                const uint32_t cnt = hd << wl;
-                for (uint32_t g = ln.id; g < cnt; g += ln.n) {
-                    uint32_t col = g & (ncols - 1), i = g >> wl;
-                    W a = at(B + i, col);
-                    W b = at(B + H + i, col);
-                    if constexpr (F::kLazy) at(B + i, col) = f.red2(a) - f.mulw(b, w) + f.p2;
-                    else at(B + i, col) = f.csub(a, f.cmulw(b, w));
-                }
+                sweep(B << wl, hd << wl, H << wl, [&](W& lo, W& hi) {
+                    if constexpr (F::kLazy) lo = f.red2(lo) - f.mulw(hi, w) + f.p2;
+                    else lo = f.csub(lo, f.cmulw(hi, w));
+                });
             }
         }
         __syncthreads();
