@@ -33,6 +33,7 @@ for d in L[-4:]:
     print(f"| {d['kernel']} | {d['gpu__time_duration.sum'] / 1e3:.1f} | {d['dram__bytes_read.sum'] / 1e6:.0f} | "
           f"{d['dram__bytes_write.sum'] / 1e6:.0f} |")
 print("\n## Config 3, p = 3221225473, n = 2^24 (tools/prof_c3.py): one forward + one inverse (c3_launches.csv)\n")
+print("(Captured before the F32 wide rounds; the current kernels at 2^24, 2^25 - 1 and 2^25 + 1 are in ncu_c3.md.)\n")
 print("| kernel | us | grid | regs | DRAM read MB | DRAM write MB | SM throughput % |\n|---|---|---|---|---|---|---|")
 for d in launches("c3_launches.csv")[:6]:
     print(f"| {d['kernel']} | {d['gpu__time_duration.sum'] / 1e3:.1f} | {d['launch__grid_size']:.0f} | "
