@@ -1,4 +1,4 @@
-tools/cu/pcie > gpurun_out/pcie.txt 2>&1
+mkdir -p tools/cu/_bin; [ -x tools/cu/_bin/pcie ] || nvcc -O2 -o tools/cu/_bin/pcie tools/cu/pcie.cu; tools/cu/_bin/pcie > gpurun_out/pcie.txt 2>&1
 python tools/prof_c2.py 512 > /dev/null 2>&1
 mkdir -p /tmp/reps
 ncu --set full --import-source on --clock-control none -k regex:"k_(clg_fwd|cli_chunks)" --launch-skip 0 --launch-count 4 -o /tmp/reps/c2 python tools/prof_c2.py 512 > gpurun_out/ncu_c2_r02.log 2>&1
