@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     if (which == 0 && h) {
         W* red = S + padded_words(1u << (L0 + WLOG));
         W* nv = red + blockDim.x;
-        colsum_pow(f, tl, K, omega_w(f, a.R, K), a.R.oneW, red, nv);
+        colsum_pow(f, tl, K, K & (0u - K), omega_w(f, a.R, K), a.R.oneW, red, nv);  // (H = K's lowest set bit)
         for (uint32_t col = threadIdx.x; col < NC; col += blockDim.x) {
             const uint32_t c = c0 + col;
             if (c >= h) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[col];
@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(256) k_col1_inv(LaunchArgs<F> a) {
     W* red = S + padded_words(1u << L0);
     W* nv = red + blockDim.x;
     TFTB_TAIL_STAMP(a, 4);
-    colsum_pow(f, tl, K, omega_w(f, a.R, K), a.R.oneW, red, nv);
+    colsum_pow(f, tl, K, K & (0u - K), omega_w(f, a.R, K), a.R.oneW, red, nv);  // (H = K's lowest set bit)
     if (threadIdx.x == 0) a.stash[(v - a.vbase) * (int64_t)C + c] = nv[0];
     TFTB_TAIL_STAMP(a, 5);
 }

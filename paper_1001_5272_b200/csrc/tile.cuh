@@ -314,20 +314,28 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
     }
 }
 
-// Per-column evaluation sum_{i<K} S[i] w^i (the first virtual output of a
-// column whose K coefficients are now known); w a canonical field word.
+// Per-column evaluation sum_{i<cnt} S[row0 + i] w^i; w a canonical field word.
 // Result per column into out[col] (canonical).  `red` is scratch of
 // blockDim.x words.  Ends synced.
+//
+// The column's next output after an in-tile solve of K known rows (its first
+// virtual word, the input of the vector's last chunk): the top-down sweep of
+// itft_phases23 leaves, in the slots [K, K + H) with H the lowest set bit of
+// K, the residue of the column modulo z^H - omega_K^H (the right child at
+// the deepest level that holds K, its coefficients in natural order), and
+// nothing writes them afterwards.  So F(omega_K) = sum_{i<H} S[K + i] omega_K^i:
+// H terms instead of the K of a Horner pass over the solved coefficients
+// (one term, no product at all, when K is odd).
 template <class F>
-TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t K, typename F::W wword,
-                        typename F::W one, typename F::W* red, typename F::W* out) {
+TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t row0, uint32_t cnt,
+                        typename F::W wword, typename F::W one, typename F::W* red, typename F::W* out) {
     using W = typename F::W;
     const uint32_t ncols = 1u << tl.wlog;
-    if (ncols >= blockDim.x) {  // wide tiles: whole columns per thread, Horner over the K rows
+    if (ncols >= blockDim.x || cnt <= 4) {  // whole columns per thread, Horner over the rows
         const Tw<W> w = f.tw(wword);
         for (uint32_t col = threadIdx.x; col < ncols; col += blockDim.x) {
             W acc = 0;
-            for (uint32_t i = K; i-- > 0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(i, col))));
+            for (uint32_t i = cnt; i-- > 0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(row0 + i, col))));
             out[col] = acc;
         }
         __syncthreads();
@@ -335,12 +343,12 @@ TFT_DEV void colsum_pow(const F& f, const SmemTile<typename F::W>& tl, uint32_t 
     }
     const uint32_t nparts = blockDim.x >> tl.wlog;
     const uint32_t col = threadIdx.x & (ncols - 1), part = threadIdx.x >> tl.wlog;
-    const uint32_t e = (K + nparts - 1) / nparts;
-    const uint32_t r0 = part * e, r1 = min(K, r0 + e);
+    const uint32_t e = (cnt + nparts - 1) / nparts;
+    const uint32_t r0 = part * e, r1 = min(cnt, r0 + e);
     const Tw<W> w = f.tw(wword);
     W acc = 0;
     if (r0 < r1) {
-        for (uint32_t i = r1; i-- > r0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(i, col))));
+        for (uint32_t i = r1; i-- > r0;) acc = f.cadd(f.cmulw(acc, w), f.canon(tl.at(tl.ix(row0 + i, col))));
         acc = f.cmulw(acc, f.tw(pow_w(f, wword, one, r0)));
     }
     red[threadIdx.x] = acc;
