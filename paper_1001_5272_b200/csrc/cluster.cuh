@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_colc_inv(LaunchArgs<F> 
     const TwPrefix<F> tpf{a.R.Zf}, tpi{a.R.Zi};
     inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, WLOG>(f, S, tpi, a.R.ipow2, rows);
     SmemTile<W> tl{S, L0, WLOG};
-    itft_phases23<WLOG>(f, tl, rows, tpf, tpi, a.R);
+    itft_phases23<WLOG>(f, tl, rows, tpf, tpi, a.R, cta_lanes(), false, true);
     // (every position of rows < rows in [lo, hi) is < n: row K only for c < h)
     col_store<F, WLOG>(f, x + c0, S, C, 0, rows, max(lo, c0) - c0, min(hi, c0 + NC) - c0);
     if (which == 0 && h) {
@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(256) k_col1_inv(LaunchArgs<F> a) {
     inv_rounds_ct<F, L0, L0, true, TwPrefix<F>, true, 0>(f, S, tpi, a.R.ipow2, K);
     TFTB_TAIL_STAMP(a, 2);
     SmemTile<W> tl{S, L0, 0};
-    itft_phases23<0>(f, tl, K, tpf, tpi, a.R);
+    itft_phases23<0>(f, tl, K, tpf, tpi, a.R, cta_lanes(), false, true);
     TFTB_TAIL_STAMP(a, 3);
     for (uint32_t r = threadIdx.x; r < K; r += blockDim.x) x[(size_t)r * C] = f.canon(S[r + (r >> 5)]);
     W* red = S + padded_words(1u << L0);

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256, kern_minb<F>()) k_tile_inv(LaunchArgs<F> 
     const TwDirect<F> tpi{a.R.Zi, 0, T, f, a.R.ZiM};
     if constexpr (T > 0) {  // (a 1-point transform is the identity)
         inv_rounds_ct<F, T, T, true>(f, S, tpi, a.R.ipow2, h, ln);
-        itft_phases23<0>(f, SmemTile<W>{S, T, 0}, h, TwDirect<F>{a.R.Zf, 0, T, f}, tpi, a.R, ln, SH::VPB > 1);
+        itft_phases23<0>(f, SmemTile<W>{S, T, 0}, h, TwDirect<F>{a.R.Zf, 0, T, f}, tpi, a.R, ln, SH::VPB > 1, true);
     }
     if (live) tile_store<W>(a.x + o, S, h, [&](W w) { return f.canon(w); }, ln);
 }

@@ -200,7 +200,7 @@ TFT_DEV void reg_inv(const F& f, typename F::W* v, uint32_t base, int slo, const
 template <int WL = -1, class F, class TPF, class TPI>
 TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32_t h, const TPF& tpf,
                       const TPI& tpi, const RingDev<typename F::W>& R, Lanes ln = cta_lanes(),
-                      bool uniform = false) {
+                      bool uniform = false, bool zero_tail = false) {
     using W = typename F::W;
     const int t = tl.t;
     const int wl = WL >= 0 ? WL : tl.wlog;
@@ -253,13 +253,23 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
             }
         }
     };
+    // zero_tail: the known tail [h, 2^t) is all zeros (a plain ITFT: every
+    // caller but the vector's last chunk).  While the block holding h still
+    // has a zero upper half, folding it into the left half is a no-op and
+    // splitting it off is a copy (w 0 = 0); the first split makes the tails
+    // nonzero.
+    bool zt = zero_tail;
     for (int d = t; d >= dlo; --d) {
         const Tw<W> w = pre ? pre2[d] : wn;
         if (!pre && act && d - 1 >= dact) wn = tw2(d - 1);
         if (d >= dact) {
             const uint32_t hd = h & ((1u << d) - 1);
             const uint32_t B = h - hd, H = 1u << (d - 1);
-            if (hd >= H) {
+            if (hd >= H && zt) {
+                const uint32_t i0 = hd - H;
+                sweep((B + i0) << wl, (H - i0) << wl, H << wl, [&](W& lo, W& hi) { hi = lo; });
+                zt = false;
+            } else if (hd >= H) {
                 const uint32_t i0 = hd - H;
                 sweep((B + i0) << wl, (H - i0) << wl, H << wl, [&](W& lo, W& hi) {
                     if constexpr (F::kLazy) {  // values stay in [0, 4p)
@@ -274,7 +284,7 @@ TFT_DEV void itft_phases23(const F& f, const SmemTile<typename F::W>& tl, uint32
                         hi = f.csub(x, m);
                     }
                 });
-            } else {
+            } else if (!zt) {
                 sweep((B + hd) << wl, (H - hd) << wl, H << wl, [&](W& lo, W& hi) {
                     if constexpr (F::kLazy) lo = f.red2(lo) + f.mulw(hi, w);
                     else lo = f.cadd(lo, f.cmulw(hi, w));
